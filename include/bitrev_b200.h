@@ -1,0 +1,146 @@
+/*
+ * bitrev_b200.h -- C ABI of libbitrev_sm100a.so, the B200 (sm_100a) bit-reversed
+ * permutation library.
+ *
+ * The permutation: for an array a of length n = 2^b, element i moves to slot
+ * rev_b(i) (rev_b reverses the low b bits of i).  It is an involution, so
+ * "dst[rev(i)] = src[i]" and "dst[i] = src[rev(i)]" are the same map.
+ *
+ * Every entry point here replaces a numba kernel (or the Python wrapper that
+ * validates and calls it) of the reference package `bitrev`
+ * (/root/reference/pkg/src/bitrev, cited as src/ below).  Those kernels take
+ * numpy arrays; the C ABI takes plain device pointers, sizes in ELEMENTS of
+ * elem_bytes bytes, and a cudaStream_t passed as void* (NULL = legacy default
+ * stream).  No torch types cross this boundary.
+ *
+ * Conventions (all entry points):
+ *   - return 0 on success;
+ *   - return a NEGATIVE BITREV_E* code for an invalid argument (nothing was
+ *     launched; the Python layer has normally raised ValueError before);
+ *   - return a POSITIVE cudaError_t value if a CUDA call failed.
+ *   - Device entry points only ENQUEUE work on `stream`: they neither allocate
+ *     nor synchronise.  The *_host entry points are synchronous (they return
+ *     when the result is in host memory), like the reference functions.
+ *   - Stateless apart from per-device caches of occupancy; safe to call from
+ *     several host threads on distinct arrays (the reference's nogil contract,
+ *     SPEC.md:253).
+ *   - elem_bytes in {1, 2, 4, 8, 16}.  4/8/16-byte elements on 16-byte aligned
+ *     pointers take the shared-memory tile kernels; anything else takes a
+ *     correct but slower element-wise kernel.
+ *   - Width domain b in [1, 48] (src/bits.py:15-23 MAX_BITS / check_width).
+ */
+#ifndef BITREV_B200_H
+#define BITREV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BITREV_OK 0
+#define BITREV_EWIDTH (-1)    /* b outside 1..48 (src/bits.py:21-23)            */
+#define BITREV_EELEM (-2)     /* elem_bytes not in {1,2,4,8,16}                  */
+#define BITREV_ENULL (-3)     /* NULL data pointer                               */
+#define BITREV_EBATCH (-4)    /* batch < 1 or a batch stride < 2^b               */
+#define BITREV_EOVERLAP (-5)  /* src/dst ranges overlap (src/permutations.py:305) */
+#define BITREV_ESHARD (-6)    /* sharded plan needs 1 <= 2g <= b_local + g       */
+#define BITREV_ETILE (-7)     /* tile-bits override not supported               */
+
+/* Library version string, e.g. "bitrev_b200 0.1.0 sm_100a". */
+const char* bitrev_version(void);
+
+/* Human-readable text for any return code above. */
+const char* bitrev_strerror(int code);
+
+/*
+ * Out-of-place permutation dst[rev_b(i)] = src[i] for `batch` independent rows.
+ * Row r of src starts at src + r*src_batch_stride elements (same for dst).
+ * Replaces: cobra_out_of_place -> _cobra_copy (src/permutations.py:293-308,
+ * 225-249); also serves oracle_permute (src/verify.py:34-39) and make_method
+ * ("cobra") (src/bench.py:164-171).  batch > 1 is an extension for the batched
+ * FFT pre-pass (BASELINE config 4); the reference handles one 1-D array.
+ * src and dst must not overlap (BITREV_EOVERLAP otherwise).
+ */
+int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
+               int64_t src_batch_stride, int64_t dst_batch_stride, void* stream);
+
+/*
+ * In-place permutation of `batch` rows of a.  Each unordered tile pair
+ * {y, rev(y)} of the middle index bits is swapped by exactly one CTA.
+ * Replaces: cobra_in_place -> _cobra_swap (src/permutations.py:311-321,
+ * 252-285), and (identical output) recursive_permute /
+ * semi_recursive_permute (src/recursive.py:189-228),
+ * parallel_semi_recursive_permute (src/parallel.py:95-156),
+ * stockham_permute, naive_bitwise_permute, bytetable_permute, xor_permute,
+ * pair_bitwise_permute (src/permutations.py:46-180) and apply_schedule with a
+ * full schedule (src/schedule.py:124-130).
+ */
+int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_stride,
+                   void* stream);
+
+/*
+ * Host-buffer variants: H2D copy into caller-provided device scratch, the
+ * kernel, D2H copy back, then stream synchronisation.  host_* may be pageable
+ * or pinned (pinned is faster).  dev_src/dev_dst (oop) and dev_buf (in-place)
+ * must each hold batch * 2^b elements.  This is the call a numpy-array caller
+ * of the reference API lands on (same functions as above).
+ */
+int bitrev_oop_host(const void* host_src, void* host_dst, int b, int elem_bytes, int64_t batch,
+                    void* dev_src, void* dev_dst, void* stream);
+int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void* dev_buf,
+                        void* stream);
+
+/*
+ * Square in-place transpose of the 2^h x 2^h row-major matrix at a
+ * (`batch` matrices, batch_stride elements apart).
+ * Replaces: transpose_square_inplace -> _transpose_diag/_transpose_offdiag
+ * (src/recursive.py:30-81).
+ */
+int bitrev_transpose_square(void* a, int h, int elem_bytes, int64_t batch, int64_t batch_stride,
+                            void* stream);
+
+/*
+ * Even-odd split out of place: dst[j] = src[2j], dst[n/2 + j] = src[2j+1].
+ * Replaces: even_odd_permute -> _even_odd (src/recursive.py:84-107); the
+ * reference runs it in place through an n/2 scratch, the Python layer does
+ * the same through a device scratch.
+ */
+int bitrev_even_odd(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
+                    int64_t src_batch_stride, int64_t dst_batch_stride, void* stream);
+
+/*
+ * Swap a[pairs[2k]] <-> a[pairs[2k+1]] for k < npairs, pairs a device array of
+ * int64 index pairs that must be pairwise disjoint (a swap schedule is).
+ * Replaces: apply_schedule -> _apply_pairs (src/schedule.py:100-130) for a
+ * caller-supplied pair list; a complete schedule takes bitrev_inplace instead.
+ */
+int bitrev_apply_pairs(void* a, const void* pairs, int64_t npairs, int elem_bytes, void* stream);
+
+/*
+ * Step 3 of the top-bit sharded plan (no reference counterpart: the reference
+ * has no multi-device path).  recv holds G = 2^g
+ * chunks of C = 2^(b_local-g) elements, chunk r received from rank r;
+ * writes dst[k*G + rev_g(r)] = recv[r*C + k].
+ */
+int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int elem_bytes,
+                          void* stream);
+
+/*
+ * Tile-bit parameter of the shared-memory kernels (the GPU analogue of
+ * CobraConfig.q, src/permutations.py:187-216; tuned like tune_cobra,
+ * src/bench.py:380-433).  Output never depends on it.  inplace selects the
+ * in-place kernel family.  set returns BITREV_ETILE if q is not instantiated
+ * for that element size; q = 0 restores the default.
+ */
+int bitrev_get_tile_bits(int elem_bytes, int inplace);
+int bitrev_set_tile_bits(int elem_bytes, int inplace, int q);
+
+/* Number of kernels this library has launched in this process (all devices). */
+int64_t bitrev_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BITREV_B200_H */

@@ -1,0 +1,507 @@
+// bitrev_capi.cu -- extern "C" entry points of libbitrev_sm100a.so (declared in
+// include/bitrev_b200.h): argument checks, kernel selection, launch geometry.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "bitrev_b200.h"
+#include "bitrev_kernels.cuh"
+
+using namespace bitrev_b200;
+
+namespace {
+
+constexpr int kMaxBits = 48;  // src/bits.py:15-18 MAX_BITS
+constexpr int kMaxDevices = 64;
+
+std::atomic<int64_t> g_launches{0};
+
+// Tile bits in use per (element size, kernel family); 0 = default.
+// Defaults chosen by measurement on B200 (see DESIGN.md / profiles/).
+std::atomic<int> g_q_oop[17];
+std::atomic<int> g_q_ip[17];
+
+int default_q(int E, bool inplace) {
+  switch (E) {
+    case 4: return 6;
+    case 8: return 5;
+    case 16: return 5;
+    default: return 0;
+  }
+  (void)inplace;
+}
+
+bool q_supported(int E, int q) {
+  switch (E) {
+    case 4: return q >= 5 && q <= 7;
+    case 8: return q >= 4 && q <= 6;
+    case 16: return q >= 3 && q <= 6;
+    default: return false;
+  }
+}
+
+int current_q(int E, bool inplace) {
+  if (E != 4 && E != 8 && E != 16) return 0;
+  const int v = inplace ? g_q_ip[E].load() : g_q_oop[E].load();
+  return v ? v : default_q(E, inplace);
+}
+
+struct DevInfo {
+  int sms = 0;
+};
+DevInfo g_dev[kMaxDevices];
+std::mutex g_dev_mu;
+
+int device_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (g_dev[dev].sms == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_dev[dev].sms = v > 0 ? v : 148;
+  }
+  return g_dev[dev].sms;
+}
+
+bool valid_elem(int E) { return E == 1 || E == 2 || E == 4 || E == 8 || E == 16; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int finish_launch() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BITREV_OK : (int)e;
+}
+
+int grid_for(uint64_t work, int per_sm, int threads_hint = 0) {
+  (void)threads_hint;
+  const uint64_t cap = (uint64_t)device_sms() * (uint64_t)(per_sm > 0 ? per_sm : 1);
+  const uint64_t g = work < cap ? work : cap;
+  return (int)(g > 0 ? g : 1);
+}
+
+// Resident CTAs per SM of a kernel at a dynamic smem size (cached per instance
+// by the caller through a function-local static).
+template <typename K>
+int occupancy(K kernel, int threads, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess)
+    n = 1;
+  return n > 0 ? n : 1;
+}
+
+// ---------------------------------------------------------------------------
+// tile launches
+
+template <int E, int Q>
+int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+                    cudaStream_t st) {
+  using T = Tile<E, Q>;
+  auto kern = bitrev_oop_tile_kernel<E, Q>;
+  static int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES);
+    return occupancy(kern, T::THREADS, T::BYTES);
+  }();
+  TileArgs a;
+  a.src = static_cast<const char*>(src);
+  a.dst = static_cast<char*>(dst);
+  a.b = b;
+  a.m = b - 2 * Q;
+  a.ntiles = (uint64_t)batch << a.m;
+  a.src_bstride = sbs * E;
+  a.dst_bstride = dbs * E;
+  a.y_begin = 0;
+  const int grid = grid_for(a.ntiles, per_sm);
+  kern<<<grid, T::THREADS, T::BYTES, st>>>(a);
+  return finish_launch();
+}
+
+template <int E, int Q>
+int launch_ip_tile(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  using T = Tile<E, Q>;
+  auto kern = bitrev_inplace_tile_kernel<E, Q>;
+  static int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * T::BYTES);
+    return occupancy(kern, T::THREADS, 2 * T::BYTES);
+  }();
+  TileArgs a;
+  a.src = static_cast<const char*>(buf);
+  a.dst = static_cast<char*>(buf);
+  a.b = b;
+  a.m = b - 2 * Q;
+  a.ntiles = (uint64_t)batch << a.m;
+  a.src_bstride = bs * E;
+  a.dst_bstride = bs * E;
+  a.y_begin = 0;
+  const int grid = grid_for(a.ntiles, per_sm);
+  kern<<<grid, T::THREADS, 2 * T::BYTES, st>>>(a);
+  return finish_launch();
+}
+
+int dispatch_oop_tile(int E, int q, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
+                      int64_t dbs, cudaStream_t st) {
+  switch (E) {
+    case 4:
+      switch (q) {
+        case 5: return launch_oop_tile<4, 5>(src, dst, b, batch, sbs, dbs, st);
+        case 6: return launch_oop_tile<4, 6>(src, dst, b, batch, sbs, dbs, st);
+        case 7: return launch_oop_tile<4, 7>(src, dst, b, batch, sbs, dbs, st);
+      }
+      break;
+    case 8:
+      switch (q) {
+        case 4: return launch_oop_tile<8, 4>(src, dst, b, batch, sbs, dbs, st);
+        case 5: return launch_oop_tile<8, 5>(src, dst, b, batch, sbs, dbs, st);
+        case 6: return launch_oop_tile<8, 6>(src, dst, b, batch, sbs, dbs, st);
+      }
+      break;
+    case 16:
+      switch (q) {
+        case 3: return launch_oop_tile<16, 3>(src, dst, b, batch, sbs, dbs, st);
+        case 4: return launch_oop_tile<16, 4>(src, dst, b, batch, sbs, dbs, st);
+        case 5: return launch_oop_tile<16, 5>(src, dst, b, batch, sbs, dbs, st);
+        case 6: return launch_oop_tile<16, 6>(src, dst, b, batch, sbs, dbs, st);
+      }
+      break;
+  }
+  return BITREV_ETILE;
+}
+
+int dispatch_ip_tile(int E, int q, void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  switch (E) {
+    case 4:
+      switch (q) {
+        case 5: return launch_ip_tile<4, 5>(buf, b, batch, bs, st);
+        case 6: return launch_ip_tile<4, 6>(buf, b, batch, bs, st);
+        case 7: return launch_ip_tile<4, 7>(buf, b, batch, bs, st);
+      }
+      break;
+    case 8:
+      switch (q) {
+        case 4: return launch_ip_tile<8, 4>(buf, b, batch, bs, st);
+        case 5: return launch_ip_tile<8, 5>(buf, b, batch, bs, st);
+        case 6: return launch_ip_tile<8, 6>(buf, b, batch, bs, st);
+      }
+      break;
+    case 16:
+      switch (q) {
+        case 3: return launch_ip_tile<16, 3>(buf, b, batch, bs, st);
+        case 4: return launch_ip_tile<16, 4>(buf, b, batch, bs, st);
+        case 5: return launch_ip_tile<16, 5>(buf, b, batch, bs, st);
+        case 6: return launch_ip_tile<16, 6>(buf, b, batch, bs, st);
+      }
+      break;
+  }
+  return BITREV_ETILE;
+}
+
+// ---------------------------------------------------------------------------
+// small / element-wise launches
+
+template <int E>
+int launch_small(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+                 cudaStream_t st) {
+  const int bytes = (1 << b) * E;
+  auto kern = bitrev_small_kernel<E>;
+  static int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallBytes);
+    return occupancy(kern, 256, kSmallBytes);
+  }();
+  const int threads = (1 << b) < 256 ? ((1 << b) < 32 ? 32 : (1 << b)) : 256;
+  const int grid = grid_for((uint64_t)batch, per_sm * (256 / threads));
+  kern<<<grid, threads, bytes, st>>>(static_cast<const char*>(src), static_cast<char*>(dst), b,
+                                     batch, sbs * E, dbs * E);
+  return finish_launch();
+}
+
+int dispatch_small(int E, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
+                   int64_t dbs, cudaStream_t st) {
+  switch (E) {
+    case 1: return launch_small<1>(src, dst, b, batch, sbs, dbs, st);
+    case 2: return launch_small<2>(src, dst, b, batch, sbs, dbs, st);
+    case 4: return launch_small<4>(src, dst, b, batch, sbs, dbs, st);
+    case 8: return launch_small<8>(src, dst, b, batch, sbs, dbs, st);
+    case 16: return launch_small<16>(src, dst, b, batch, sbs, dbs, st);
+  }
+  return BITREV_EELEM;
+}
+
+uint64_t elementwise_grid(uint64_t total) {
+  const uint64_t blocks = (total + 255) / 256;
+  const uint64_t cap = (uint64_t)device_sms() * 8;
+  return blocks < cap ? (blocks ? blocks : 1) : cap;
+}
+
+template <int E>
+int launch_gather(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+                  cudaStream_t st) {
+  const uint64_t total = (1ull << b) * (uint64_t)batch;
+  bitrev_gather_kernel<E><<<(unsigned)elementwise_grid(total), 256, 0, st>>>(
+      static_cast<const char*>(src), static_cast<char*>(dst), b, batch, sbs * E, dbs * E);
+  return finish_launch();
+}
+
+int dispatch_gather(int E, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
+                    int64_t dbs, cudaStream_t st) {
+  switch (E) {
+    case 1: return launch_gather<1>(src, dst, b, batch, sbs, dbs, st);
+    case 2: return launch_gather<2>(src, dst, b, batch, sbs, dbs, st);
+    case 4: return launch_gather<4>(src, dst, b, batch, sbs, dbs, st);
+    case 8: return launch_gather<8>(src, dst, b, batch, sbs, dbs, st);
+    case 16: return launch_gather<16>(src, dst, b, batch, sbs, dbs, st);
+  }
+  return BITREV_EELEM;
+}
+
+template <int E>
+int launch_swap(void* a, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  const uint64_t total = (1ull << b) * (uint64_t)batch;
+  bitrev_swap_kernel<E><<<(unsigned)elementwise_grid(total), 256, 0, st>>>(
+      static_cast<char*>(a), b, batch, bs * E);
+  return finish_launch();
+}
+
+int dispatch_swap(int E, void* a, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  switch (E) {
+    case 1: return launch_swap<1>(a, b, batch, bs, st);
+    case 2: return launch_swap<2>(a, b, batch, bs, st);
+    case 4: return launch_swap<4>(a, b, batch, bs, st);
+    case 8: return launch_swap<8>(a, b, batch, bs, st);
+    case 16: return launch_swap<16>(a, b, batch, bs, st);
+  }
+  return BITREV_EELEM;
+}
+
+int check_common(int b, int E, int64_t batch) {
+  if (b < 1 || b > kMaxBits) return BITREV_EWIDTH;
+  if (!valid_elem(E)) return BITREV_EELEM;
+  if (batch < 1) return BITREV_EBATCH;
+  return BITREV_OK;
+}
+
+// Pick the tile bits for (E, b): the configured q, reduced so that 2q <= b.
+int pick_q(int E, int b, bool inplace) {
+  int q = current_q(E, inplace);
+  while (q > 0 && 2 * q > b) --q;
+  return q_supported(E, q) ? q : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bitrev_version(void) { return "bitrev_b200 0.1.0 sm_100a"; }
+
+const char* bitrev_strerror(int code) {
+  switch (code) {
+    case BITREV_OK: return "ok";
+    case BITREV_EWIDTH: return "bit width must be in 1..48";
+    case BITREV_EELEM: return "element size must be 1, 2, 4, 8 or 16 bytes";
+    case BITREV_ENULL: return "null data pointer";
+    case BITREV_EBATCH: return "batch must be >= 1 and batch strides >= 2**b";
+    case BITREV_EOVERLAP: return "source and dest must not overlap";
+    case BITREV_ESHARD: return "sharded plan needs 2g <= b (global width)";
+    case BITREV_ETILE: return "tile bits not instantiated for this element size";
+  }
+  if (code > 0) return cudaGetErrorString(static_cast<cudaError_t>(code));
+  return "unknown bitrev error";
+}
+
+int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
+               int64_t src_batch_stride, int64_t dst_batch_stride, void* stream) {
+  const int E = elem_bytes;
+  int rc = check_common(b, E, batch);
+  if (rc) return rc;
+  if (!src || !dst) return BITREV_ENULL;
+  const int64_t n = int64_t(1) << b;
+  if (batch > 1 && (src_batch_stride < n || dst_batch_stride < n)) return BITREV_EBATCH;
+  if (batch == 1) src_batch_stride = dst_batch_stride = n;
+  {
+    const uintptr_t s0 = (uintptr_t)src, d0 = (uintptr_t)dst;
+    const uintptr_t s1 = s0 + (uintptr_t)((batch - 1) * src_batch_stride + n) * E;
+    const uintptr_t d1 = d0 + (uintptr_t)((batch - 1) * dst_batch_stride + n) * E;
+    if (s0 < d1 && d0 < s1) return BITREV_EOVERLAP;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n * E <= kSmallBytes) return dispatch_small(E, src, dst, b, batch, src_batch_stride,
+                                                   dst_batch_stride, st);
+  const int q = pick_q(E, b, false);
+  const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
+                      ((dst_batch_stride * E) % 16 == 0);
+  if (q && vec_ok)
+    return dispatch_oop_tile(E, q, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
+  return dispatch_gather(E, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
+}
+
+int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_stride,
+                   void* stream) {
+  const int E = elem_bytes;
+  int rc = check_common(b, E, batch);
+  if (rc) return rc;
+  if (!a) return BITREV_ENULL;
+  const int64_t n = int64_t(1) << b;
+  if (batch > 1 && batch_stride < n) return BITREV_EBATCH;
+  if (batch == 1) batch_stride = n;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n * E <= kSmallBytes) return dispatch_small(E, a, a, b, batch, batch_stride, batch_stride, st);
+  const int q = pick_q(E, b, true);
+  const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
+  if (q && vec_ok) return dispatch_ip_tile(E, q, a, b, batch, batch_stride, st);
+  return dispatch_swap(E, a, b, batch, batch_stride, st);
+}
+
+int bitrev_oop_host(const void* host_src, void* host_dst, int b, int elem_bytes, int64_t batch,
+                    void* dev_src, void* dev_dst, void* stream) {
+  int rc = check_common(b, elem_bytes, batch);
+  if (rc) return rc;
+  if (!host_src || !host_dst || !dev_src || !dev_dst) return BITREV_ENULL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
+  cudaError_t e = cudaMemcpyAsync(dev_src, host_src, bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t n = int64_t(1) << b;
+  rc = bitrev_oop(dev_src, dev_dst, b, elem_bytes, batch, n, n, stream);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(host_dst, dev_dst, bytes, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? BITREV_OK : (int)e;
+}
+
+int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void* dev_buf,
+                        void* stream) {
+  int rc = check_common(b, elem_bytes, batch);
+  if (rc) return rc;
+  if (!host_a || !dev_buf) return BITREV_ENULL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
+  cudaError_t e = cudaMemcpyAsync(dev_buf, host_a, bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t n = int64_t(1) << b;
+  rc = bitrev_inplace(dev_buf, b, elem_bytes, batch, n, stream);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(host_a, dev_buf, bytes, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? BITREV_OK : (int)e;
+}
+
+int bitrev_transpose_square(void* a, int h, int elem_bytes, int64_t batch, int64_t batch_stride,
+                            void* stream) {
+  if (h < 0 || 2 * h > kMaxBits) return BITREV_EWIDTH;
+  if (!valid_elem(elem_bytes)) return BITREV_EELEM;
+  if (batch < 1) return BITREV_EBATCH;
+  if (!a) return BITREV_ENULL;
+  const int64_t n = int64_t(1) << (2 * h);
+  if (batch > 1 && batch_stride < n) return BITREV_EBATCH;
+  if (batch == 1) batch_stride = n;
+  if (h == 0) return BITREV_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int side = 1 << h;
+  const int ts = side < kTT ? side : kTT;
+  const uint64_t nt = (uint64_t)(side / ts);
+  const uint64_t work = nt * nt * (uint64_t)batch;
+  const int grid = grid_for(work, 6);
+  switch (elem_bytes) {
+#define TR_CASE(E)                                                                        \
+  case E:                                                                                 \
+    transpose_square_kernel<E><<<grid, 256, 0, st>>>(static_cast<char*>(a), h, batch,     \
+                                                     batch_stride * E);                   \
+    return finish_launch();
+    TR_CASE(1) TR_CASE(2) TR_CASE(4) TR_CASE(8) TR_CASE(16)
+#undef TR_CASE
+  }
+  return BITREV_EELEM;
+}
+
+int bitrev_even_odd(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
+                    int64_t src_batch_stride, int64_t dst_batch_stride, void* stream) {
+  const int E = elem_bytes;
+  int rc = check_common(b, E, batch);
+  if (rc) return rc;
+  if (!src || !dst) return BITREV_ENULL;
+  const int64_t n = int64_t(1) << b;
+  if (batch > 1 && (src_batch_stride < n || dst_batch_stride < n)) return BITREV_EBATCH;
+  if (batch == 1) src_batch_stride = dst_batch_stride = n;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t total = (uint64_t)(n / 2) * (uint64_t)batch;
+  const unsigned grid = (unsigned)elementwise_grid(total);
+  switch (E) {
+#define EO_CASE(E_)                                                                          \
+  case E_:                                                                                   \
+    even_odd_kernel<E_><<<grid, 256, 0, st>>>(static_cast<const char*>(src),                  \
+                                              static_cast<char*>(dst), b, batch,              \
+                                              src_batch_stride * E_, dst_batch_stride * E_); \
+    return finish_launch();
+    EO_CASE(1) EO_CASE(2) EO_CASE(4) EO_CASE(8) EO_CASE(16)
+#undef EO_CASE
+  }
+  return BITREV_EELEM;
+}
+
+int bitrev_apply_pairs(void* a, const void* pairs, int64_t npairs, int elem_bytes, void* stream) {
+  if (!valid_elem(elem_bytes)) return BITREV_EELEM;
+  if (npairs < 0) return BITREV_EBATCH;
+  if (npairs == 0) return BITREV_OK;
+  if (!a || !pairs) return BITREV_ENULL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned grid = (unsigned)elementwise_grid((uint64_t)npairs);
+  const long long* pr = static_cast<const long long*>(pairs);
+  switch (elem_bytes) {
+#define AP_CASE(E_)                                                                  \
+  case E_:                                                                           \
+    apply_pairs_kernel<E_><<<grid, 256, 0, st>>>(static_cast<char*>(a), pr, npairs); \
+    return finish_launch();
+    AP_CASE(1) AP_CASE(2) AP_CASE(4) AP_CASE(8) AP_CASE(16)
+#undef AP_CASE
+  }
+  return BITREV_EELEM;
+}
+
+int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int elem_bytes,
+                          void* stream) {
+  const int E = elem_bytes;
+  if (b_local < 1 || b_local > kMaxBits) return BITREV_EWIDTH;
+  if (!valid_elem(E)) return BITREV_EELEM;
+  if (g < 0 || g > b_local) return BITREV_ESHARD;
+  if (!recv || !dst) return BITREV_ENULL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t C = 1ull << (b_local - g);
+  const unsigned grid = (unsigned)elementwise_grid(C);
+  const char* r = static_cast<const char*>(recv);
+  char* d = static_cast<char*>(dst);
+#define UNPACK_G(E_, G_)                                            \
+  case G_:                                                          \
+    sharded_unpack_kernel<E_, G_><<<grid, 256, 0, st>>>(r, d, C);   \
+    return finish_launch();
+#define UNPACK_E(E_)                                                                     \
+  case E_:                                                                               \
+    switch (1 << g) {                                                                    \
+      UNPACK_G(E_, 1) UNPACK_G(E_, 2) UNPACK_G(E_, 4) UNPACK_G(E_, 8)                    \
+      default:                                                                           \
+        sharded_unpack_generic_kernel<E_><<<(unsigned)elementwise_grid(C << g), 256, 0,  \
+                                            st>>>(r, d, C, g);                           \
+        return finish_launch();                                                          \
+    }
+  switch (E) { UNPACK_E(1) UNPACK_E(2) UNPACK_E(4) UNPACK_E(8) UNPACK_E(16) }
+#undef UNPACK_E
+#undef UNPACK_G
+  return BITREV_EELEM;
+}
+
+int bitrev_get_tile_bits(int elem_bytes, int inplace) { return current_q(elem_bytes, inplace != 0); }
+
+int bitrev_set_tile_bits(int elem_bytes, int inplace, int q) {
+  if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16) return BITREV_ETILE;
+  if (q != 0 && !q_supported(elem_bytes, q)) return BITREV_ETILE;
+  (inplace ? g_q_ip : g_q_oop)[elem_bytes].store(q);
+  return BITREV_OK;
+}
+
+int64_t bitrev_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

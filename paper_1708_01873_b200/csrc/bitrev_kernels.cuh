@@ -1,0 +1,463 @@
+// bitrev_kernels.cuh -- sm_100a kernels for the bit-reversed permutation.
+//
+// Index model (the COBRA split of src/permutations.py:225-249):
+//   i = x * 2^(b-Q) + y * 2^Q + z,   x, z in [0, 2^Q),  y in [0, 2^m),  m = b - 2Q
+//   rev_b(i) = rev_Q(z) * 2^(b-Q) + rev_m(y) * 2^Q + rev_Q(x)
+// For a fixed middle value y the 2^Q x 2^Q elements {x, z} form one "tile": 2^Q
+// source rows of 2^Q contiguous elements (stride 2^(b-Q)), landing in 2^Q
+// destination rows of 2^Q contiguous elements inside the rev(y) slab.  A tile is
+// the paper's square transposition with the rows and columns
+// also bit-reversed; it is staged through shared memory so BOTH the global reads
+// and the global writes are 16-byte vectors over contiguous 2^Q*E-byte runs.
+//
+// Data path per tile (E = element bytes, V = 16/E elements per 16-byte vector):
+//   1. each thread issues V LDG.128 from rows x_k = g + k*2^Q/V (k < V) at the
+//      same 16-byte column c.  Because rev_Q(x_k) = rev(g)*V + rev_LV(k), those V
+//      rows are exactly one aligned group of V destination positions;
+//   2. a V x V register transpose turns them into V vectors, one per source
+//      column z = c*V + j, each already holding V consecutive destination
+//      elements in destination order;
+//   3. STS.128 into U[z][rev(g)] (shared memory, XOR-swizzled 16-byte chunks:
+//      chunk' = chunk ^ ((z/V) & 7), bank-conflict free on both sides);
+//   4. after a barrier, each thread reads a contiguous chunk of row z of U
+//      (LDS.128) and writes it to destination row rev_Q(z) (STG.128).
+// The persistent loop issues the next tile's loads before draining the current
+// one, so every warp keeps V*IPT 16-byte loads in flight across the drain.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bitrev_b200 {
+
+// ---------------------------------------------------------------------------
+// bit helpers
+
+// Reverse the low w bits of v (0 <= w <= 64); rev of width 0 is 0.  Replaces
+// rev_naive (src/bits.py:31-47) -- one BREV pair instead of a w-step loop.
+__device__ __forceinline__ uint64_t dev_rev(uint64_t v, int w) {
+  return w <= 0 ? 0ull : (__brevll(v) >> (64 - w));
+}
+
+__host__ __device__ constexpr int const_rev(int v, int w) {
+  return w == 0 ? 0 : (((v & 1) << (w - 1)) | const_rev(v >> 1, w - 1));
+}
+
+__host__ __device__ constexpr int const_log2(int v) { return v <= 1 ? 0 : 1 + const_log2(v >> 1); }
+
+template <int E> struct Word;
+template <> struct Word<1> { using T = uint8_t; };
+template <> struct Word<2> { using T = uint16_t; };
+template <> struct Word<4> { using T = uint32_t; };
+template <> struct Word<8> { using T = unsigned long long; };
+template <> struct Word<16> { using T = uint4; };
+
+// 128-bit global accesses.  Source rows are read exactly once per launch, so the
+// loads bypass L1 allocation; stores are plain (the permuted array is normally
+// consumed next, e.g. by the first FFT butterfly stage, so keep it in L2).
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_plain(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_vec(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// tile geometry
+
+template <int E, int Q>
+struct Tile {
+  static constexpr int S = 1 << Q;           // tile side (elements)
+  static constexpr int V = 16 / E;           // elements per 16-byte vector
+  static constexpr int LV = const_log2(V);
+  static constexpr int CH = S / V;           // 16-byte chunks per tile row
+  static constexpr int ITEMS = CH * CH;      // load items (V loads each)
+  static constexpr int WCH = S * CH;         // 16-byte chunks per tile
+  static constexpr int THREADS = ITEMS < 256 ? ITEMS : 256;
+  static constexpr int IPT = ITEMS / THREADS;  // load items per thread
+  static constexpr int WPT = WCH / THREADS;    // drain chunks per thread
+  static constexpr int BYTES = S * S * E;
+  static_assert(E == 4 || E == 8 || E == 16, "tile kernels move 4/8/16-byte elements");
+  static_assert(CH >= 8, "XOR swizzle needs >= 8 chunks per row");
+  static_assert(ITEMS % THREADS == 0 && WCH % THREADS == 0, "even split");
+};
+
+// Shared-memory chunk index of (row z, chunk col) with the 3-bit XOR swizzle.
+template <int E, int Q>
+__device__ __forceinline__ int swz(int z, int col) {
+  using T = Tile<E, Q>;
+  return z * T::CH + (col ^ ((z >> T::LV) & 7));
+}
+
+// Issue the V*IPT loads of one tile (rows at stride row_stride bytes).
+template <int E, int Q, bool STREAM>
+__device__ __forceinline__ void tile_load(uint4 (&r)[Tile<E, Q>::IPT][Tile<E, Q>::V],
+                                          const char* tile_base, uint64_t row_stride) {
+  using T = Tile<E, Q>;
+#pragma unroll
+  for (int it = 0; it < T::IPT; ++it) {
+    const int id = it * T::THREADS + threadIdx.x;
+    const int c = id % T::CH;
+    const int g = id / T::CH;
+#pragma unroll
+    for (int k = 0; k < T::V; ++k) {
+      const char* p = tile_base + (uint64_t)(g + k * T::CH) * row_stride + (uint64_t)c * 16;
+      r[it][k] = STREAM ? ld_stream(p) : ld_plain(p);
+    }
+  }
+}
+
+// Component j of a uint4 (j is a compile-time constant after unrolling).
+template <int J>
+__device__ __forceinline__ uint32_t comp(const uint4& v) {
+  if constexpr (J == 0) return v.x;
+  else if constexpr (J == 1) return v.y;
+  else if constexpr (J == 2) return v.z;
+  else return v.w;
+}
+
+// V x V transpose in registers: out[j] holds source column c*V+j for the V rows
+// k, element slot rev_LV(k).  E=16 is the identity; E=8 swaps 64-bit halves;
+// E=4 is a 4x4 word transpose with rows in bit-reversed order (0,2,1,3).
+template <int E, int J>
+__device__ __forceinline__ uint4 xpose(const uint4 (&a)[16 / E]) {
+  if constexpr (E == 16) {
+    return a[0];
+  } else if constexpr (E == 8) {
+    if constexpr (J == 0) return make_uint4(a[0].x, a[0].y, a[1].x, a[1].y);
+    else return make_uint4(a[0].z, a[0].w, a[1].z, a[1].w);
+  } else {
+    return make_uint4(comp<J>(a[0]), comp<J>(a[2]), comp<J>(a[1]), comp<J>(a[3]));
+  }
+}
+
+template <int E, int Q, int J>
+__device__ __forceinline__ void stage_col(const uint4 (&a)[16 / E], uint4* U, int c, int col) {
+  using T = Tile<E, Q>;
+  if constexpr (J < T::V) {
+    U[swz<E, Q>(c * T::V + J, col)] = xpose<E, J>(a);
+    stage_col<E, Q, J + 1>(a, U, c, col);
+  }
+}
+
+// Register transpose + swizzled STS of one tile into U.
+template <int E, int Q>
+__device__ __forceinline__ void tile_stage(const uint4 (&r)[Tile<E, Q>::IPT][Tile<E, Q>::V],
+                                           uint4* U) {
+  using T = Tile<E, Q>;
+#pragma unroll
+  for (int it = 0; it < T::IPT; ++it) {
+    const int id = it * T::THREADS + threadIdx.x;
+    const int c = id % T::CH;
+    const int g = id / T::CH;
+    const int col = (int)(__brev((unsigned)g) >> (32 - (Q - T::LV)));  // rev_{Q-LV}(g)
+    stage_col<E, Q, 0>(r[it], U, c, col);
+  }
+}
+
+// Drain U: row z goes to destination row rev_Q(z) (stride row_stride bytes).
+template <int E, int Q>
+__device__ __forceinline__ void tile_drain(const uint4* U, char* dst_base, uint64_t row_stride) {
+  using T = Tile<E, Q>;
+#pragma unroll
+  for (int it = 0; it < T::WPT; ++it) {
+    const int id = it * T::THREADS + threadIdx.x;
+    const int col = id % T::CH;
+    const int z = id / T::CH;
+    const uint4 v = U[swz<E, Q>(z, col)];
+    const uint64_t rz = __brev((unsigned)z) >> (32 - Q);
+    st_vec(dst_base + rz * row_stride + (uint64_t)col * 16, v);
+  }
+}
+
+struct TileArgs {
+  const char* src;
+  char* dst;
+  int b;               // index bits
+  int m;               // middle bits b - 2Q
+  uint64_t ntiles;     // batch << m (oop) or batch << m (in-place, incl. skipped)
+  int64_t src_bstride; // bytes between batch rows
+  int64_t dst_bstride;
+  uint64_t y_begin;    // first middle value (host-staged chunking); usually 0
+};
+
+// ---------------------------------------------------------------------------
+// out-of-place tile kernel (replaces _cobra_copy, src/permutations.py:225-249)
+
+template <int E, int Q>
+__global__ void __launch_bounds__(Tile<E, Q>::THREADS)
+    bitrev_oop_tile_kernel(TileArgs a) {
+  using T = Tile<E, Q>;
+  extern __shared__ __align__(16) uint4 smem[];
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t mmask = (1ull << a.m) - 1;
+  uint4 r[T::IPT][T::V];
+
+  uint64_t t = blockIdx.x;
+  if (t >= a.ntiles) return;
+  auto src_tile = [&](uint64_t tt) {
+    const uint64_t bi = tt >> a.m, y = (tt & mmask) + a.y_begin;
+    return a.src + bi * a.src_bstride + (y << Q) * E;
+  };
+  tile_load<E, Q, true>(r, src_tile(t), row_stride);
+  for (;;) {
+    const uint64_t bi = t >> a.m, y = (t & mmask) + a.y_begin;
+    tile_stage<E, Q>(r, smem);
+    __syncthreads();
+    const uint64_t tn = t + gridDim.x;
+    if (tn < a.ntiles) tile_load<E, Q, true>(r, src_tile(tn), row_stride);
+    char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << Q) * E;
+    tile_drain<E, Q>(smem, dbase, row_stride);
+    if (tn >= a.ntiles) break;
+    __syncthreads();
+    t = tn;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// in-place tile-pair kernel (replaces _cobra_swap, src/permutations.py:252-285)
+//
+// Work item y (per batch row) with y <= rev(y): load tile y and tile rev(y) into
+// two shared buffers, barrier, write tile y's data into the rev(y) slab and
+// tile rev(y)'s data into the y slab.  A palindromic y (y == rev(y)) is loaded
+// and written back transposed alone.  Items with rev(y) < y are skipped -- each
+// unordered pair is handled exactly once (src/permutations.py:263-264), so no
+// two CTAs ever touch the same element and both tiles are resident before the
+// first write.
+
+template <int E, int Q>
+__global__ void __launch_bounds__(Tile<E, Q>::THREADS)
+    bitrev_inplace_tile_kernel(TileArgs a) {
+  using T = Tile<E, Q>;
+  extern __shared__ __align__(16) uint4 smem[];
+  uint4* U0 = smem;
+  uint4* U1 = smem + T::WCH;
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t mmask = (1ull << a.m) - 1;
+  uint4 r0[T::IPT][T::V], r1[T::IPT][T::V];
+
+  // next work item at or after tt with y <= rev(y)
+  auto advance = [&](uint64_t tt) {
+    while (tt < a.ntiles) {
+      const uint64_t y = tt & mmask;
+      if (dev_rev(y, a.m) >= y) break;
+      tt += gridDim.x;
+    }
+    return tt;
+  };
+  auto issue = [&](uint64_t tt) {
+    const uint64_t bi = tt >> a.m, y = tt & mmask, ry = dev_rev(y, a.m);
+    const char* base = a.src + bi * a.src_bstride;
+    tile_load<E, Q, false>(r0, base + (y << Q) * E, row_stride);
+    if (ry != y) tile_load<E, Q, false>(r1, base + (ry << Q) * E, row_stride);
+  };
+
+  uint64_t t = advance(blockIdx.x);
+  if (t >= a.ntiles) return;
+  issue(t);
+  for (;;) {
+    const uint64_t bi = t >> a.m, y = t & mmask, ry = dev_rev(y, a.m);
+    const bool pair = ry != y;
+    tile_stage<E, Q>(r0, U0);
+    if (pair) tile_stage<E, Q>(r1, U1);
+    __syncthreads();
+    const uint64_t tn = advance(t + gridDim.x);
+    if (tn < a.ntiles) issue(tn);
+    char* base = a.dst + bi * a.dst_bstride;
+    tile_drain<E, Q>(U0, base + (ry << Q) * E, row_stride);
+    if (pair) tile_drain<E, Q>(U1, base + (y << Q) * E, row_stride);
+    if (tn >= a.ntiles) break;
+    __syncthreads();
+    t = tn;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// whole-row-in-shared-memory kernel for small n (n*E <= kSmallBytes); one CTA
+// per batch row, grid-stride over rows.  Works in place (src == dst) because
+// every read of a row precedes the barrier and every write follows it.
+
+constexpr int kSmallBytes = 32 * 1024;
+
+template <int E>
+__global__ void __launch_bounds__(256)
+    bitrev_small_kernel(const char* src, char* dst, int b, int64_t batch, int64_t src_bstride,
+                        int64_t dst_bstride) {
+  using W = typename Word<E>::T;
+  extern __shared__ __align__(16) uint4 smem_raw[];
+  W* buf = reinterpret_cast<W*>(smem_raw);
+  const int n = 1 << b;
+  for (int64_t row = blockIdx.x; row < batch; row += gridDim.x) {
+    const W* s = reinterpret_cast<const W*>(src + row * src_bstride);
+    W* d = reinterpret_cast<W*>(dst + row * dst_bstride);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) buf[i] = s[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = buf[dev_rev((uint64_t)i, b)];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// element-wise fallbacks (unaligned pointers, 1/2-byte elements): correct for
+// every width, not bandwidth-optimal.
+
+template <int E>
+__global__ void bitrev_gather_kernel(const char* src, char* dst, int b, int64_t batch,
+                                     int64_t src_bstride, int64_t dst_bstride) {
+  using W = typename Word<E>::T;
+  const uint64_t n = 1ull << b;
+  const uint64_t total = n * (uint64_t)batch;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = t >> b, i = t & (n - 1);
+    const W* s = reinterpret_cast<const W*>(src + row * src_bstride);
+    W* d = reinterpret_cast<W*>(dst + row * dst_bstride);
+    d[i] = s[dev_rev(i, b)];
+  }
+}
+
+// Swap a[i] <-> a[rev(i)] for i < rev(i): the data-parallel form of
+// _naive_bitwise (src/permutations.py:66-78); each pair is owned by one thread.
+template <int E>
+__global__ void bitrev_swap_kernel(char* a, int b, int64_t batch, int64_t bstride) {
+  using W = typename Word<E>::T;
+  const uint64_t n = 1ull << b;
+  const uint64_t total = n * (uint64_t)batch;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = t >> b, i = t & (n - 1);
+    const uint64_t r = dev_rev(i, b);
+    if (i < r) {
+      W* p = reinterpret_cast<W*>(a + row * bstride);
+      const W tmp = p[i];
+      p[i] = p[r];
+      p[r] = tmp;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// square in-place transpose (replaces _transpose_diag/_transpose_offdiag,
+// src/recursive.py:30-81): tile pair {(I,J),(J,I)}, I <= J, per CTA-iteration.
+
+constexpr int kTT = 32;  // transpose tile side
+
+template <int E>
+__global__ void __launch_bounds__(256)
+    transpose_square_kernel(char* a, int h, int64_t batch, int64_t bstride) {
+  using W = typename Word<E>::T;
+  __shared__ W t0[kTT][kTT + 1];
+  __shared__ W t1[kTT][kTT + 1];
+  const int side = 1 << h;
+  const int ts = side < kTT ? side : kTT;
+  const int nt = side / ts;  // tiles per dimension
+  const uint64_t per = (uint64_t)nt * nt;
+  const uint64_t total = per * (uint64_t)batch;
+  const int tx = threadIdx.x % kTT, ty = threadIdx.x / kTT;  // 32 x 8
+  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    const uint64_t bi = w / per;
+    const uint64_t rem = w % per;
+    const int I = (int)(rem / nt), J = (int)(rem % nt);
+    if (I > J) continue;  // block-uniform
+    W* m = reinterpret_cast<W*>(a + bi * bstride);
+    for (int r = ty; r < ts; r += 8)
+      if (tx < ts) {
+        t0[r][tx] = m[(uint64_t)(I * ts + r) * side + J * ts + tx];
+        if (I != J) t1[r][tx] = m[(uint64_t)(J * ts + r) * side + I * ts + tx];
+      }
+    __syncthreads();
+    for (int r = ty; r < ts; r += 8)
+      if (tx < ts) {
+        m[(uint64_t)(J * ts + r) * side + I * ts + tx] = t0[tx][r];
+        if (I != J) m[(uint64_t)(I * ts + r) * side + J * ts + tx] = t1[tx][r];
+      }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// even-odd split (replaces _even_odd, src/recursive.py:84-93), out of place.
+
+template <int E>
+__global__ void even_odd_kernel(const char* src, char* dst, int b, int64_t batch,
+                                int64_t src_bstride, int64_t dst_bstride) {
+  using W = typename Word<E>::T;
+  const uint64_t half = 1ull << (b - 1);
+  const uint64_t total = half * (uint64_t)batch;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = t / half, j = t % half;
+    const W* s = reinterpret_cast<const W*>(src + row * src_bstride);
+    W* d = reinterpret_cast<W*>(dst + row * dst_bstride);
+    const W e = s[2 * j], o = s[2 * j + 1];
+    d[j] = e;
+    d[half + j] = o;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// explicit pair list (replaces _apply_pairs, src/schedule.py:100-107); pairs are
+// disjoint, so one thread per pair needs no synchronisation.
+
+template <int E>
+__global__ void apply_pairs_kernel(char* a, const long long* pairs, int64_t npairs) {
+  using W = typename Word<E>::T;
+  W* p = reinterpret_cast<W*>(a);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < npairs;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const long long i = pairs[2 * k], j = pairs[2 * k + 1];
+    const W t = p[i];
+    p[i] = p[j];
+    p[j] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sharded plan, step 3: dst[k*G + rev_g(r)] = recv[r*C + k].
+// One thread per k gathers the G values (coalesced across threads in k) and
+// writes its G*E contiguous destination bytes.
+
+template <int E, int G>
+__global__ void sharded_unpack_kernel(const char* recv, char* dst, uint64_t C) {
+  using W = typename Word<E>::T;
+  constexpr int LG = const_log2(G);
+  const W* rv = reinterpret_cast<const W*>(recv);
+  W* d = reinterpret_cast<W*>(dst);
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < C;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    W v[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) v[const_rev(r, LG)] = rv[(uint64_t)r * C + k];
+#pragma unroll
+    for (int s = 0; s < G; ++s) d[k * G + s] = v[s];
+  }
+}
+
+template <int E>
+__global__ void sharded_unpack_generic_kernel(const char* recv, char* dst, uint64_t C, int g) {
+  using W = typename Word<E>::T;
+  const W* rv = reinterpret_cast<const W*>(recv);
+  W* d = reinterpret_cast<W*>(dst);
+  const uint64_t G = 1ull << g;
+  const uint64_t total = C * G;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = t / C, k = t % C;
+    d[k * G + dev_rev(r, g)] = rv[t];
+  }
+}
+
+}  // namespace bitrev_b200

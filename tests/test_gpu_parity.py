@@ -1,0 +1,168 @@
+"""GPU parity: every kernel path vs the CPU oracle, byte for byte.
+
+Inputs are seeded random BIT PATTERNS (numpy default_rng bytes), so any
+misplaced element, torn vector or swapped half shows up; comparison is on the
+raw bytes (np.array_equal would hide -0.0/NaN differences).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1708_01873_b200 as br
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+DTYPES = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64, 16: torch.complex128}
+NP_DTYPES = {1: np.uint8, 2: np.int16, 4: np.int32, 8: np.int64, 16: np.complex128}
+
+
+def rand_bits(n, E, seed, batch=None):
+    rng = np.random.default_rng(seed)
+    shape = (n,) if batch is None else (batch, n)
+    raw = rng.integers(0, 256, size=(int(np.prod(shape)) * E,), dtype=np.uint8)
+    return raw.view(NP_DTYPES[E]).reshape(shape)
+
+
+def as_bytes(x):
+    if isinstance(x, torch.Tensor):
+        x = x.detach().cpu().contiguous().numpy()
+    return np.ascontiguousarray(x).view(np.uint8)
+
+
+def assert_same(got, expected):
+    g, e = as_bytes(got), as_bytes(expected)
+    assert g.shape == e.shape
+    if not np.array_equal(g, e):
+        bad = np.nonzero(g != e)[0]
+        pytest.fail(f"{bad.size} bytes differ, first at byte {bad[:4].tolist()}")
+
+
+WIDTHS = list(range(1, 23))
+
+
+@pytest.mark.parametrize("E", [4, 8, 16, 2, 1])
+@pytest.mark.parametrize("b", WIDTHS)
+def test_oop_matches_oracle(cuda, E, b):
+    host = rand_bits(1 << b, E, seed=1000 * E + b)
+    src = torch.from_numpy(host).to(cuda)
+    dst = torch.empty_like(src)
+    br.cobra_out_of_place(src, dst, br.CobraConfig(br.default_cobra_q(b)), b)
+    torch.cuda.synchronize()
+    assert_same(dst, orc.oracle_permute(host, b))
+    assert_same(src, host)  # source never written
+
+
+@pytest.mark.parametrize("E", [4, 8, 16, 2, 1])
+@pytest.mark.parametrize("b", WIDTHS)
+def test_inplace_matches_oracle(cuda, E, b):
+    host = rand_bits(1 << b, E, seed=2000 * E + b)
+    a = torch.from_numpy(host).to(cuda)
+    br.cobra_in_place(a, br.CobraConfig(br.default_cobra_q(b)), b)
+    torch.cuda.synchronize()
+    assert_same(a, orc.oracle_permute(host, b))
+
+
+@pytest.mark.parametrize("E", [4, 8, 16])
+@pytest.mark.parametrize("b", [16, 17, 20, 21])
+def test_every_tile_size(cuda, E, b):
+    """Every instantiated tile width Q gives the same bytes (output never
+    depends on the tile parameter, like CobraConfig.q)."""
+    host = rand_bits(1 << b, E, seed=3000 * E + b)
+    expected = orc.oracle_permute(host, b)
+    qs = {4: [5, 6, 7], 8: [4, 5, 6], 16: [3, 4, 5, 6]}[E]
+    try:
+        for q in qs:
+            for inplace in (False, True):
+                br.set_tile_bits(E, inplace, q)
+            src = torch.from_numpy(host).to(cuda)
+            dst = torch.empty_like(src)
+            br.cobra_out_of_place(src, dst, br.CobraConfig(0), b)
+            br.cobra_in_place(src, br.CobraConfig(0), b)
+            torch.cuda.synchronize()
+            assert_same(dst, expected)
+            assert_same(src, expected)
+    finally:
+        for inplace in (False, True):
+            br.set_tile_bits(E, inplace, 0)
+
+
+@pytest.mark.parametrize("E", [4, 8, 16])
+@pytest.mark.parametrize("b,batch", [(3, 5), (10, 7), (13, 3), (16, 9)])
+def test_batched(cuda, E, b, batch):
+    host = rand_bits(1 << b, E, seed=4000 * E + b, batch=batch)
+    src = torch.from_numpy(host).to(cuda)
+    out = br.bitrev_batched(src, b)
+    ip = src.clone()
+    br.bitrev_batched_inplace(ip, b)
+    torch.cuda.synchronize()
+    expected = orc.oracle_permute(host, b)
+    assert_same(out, expected)
+    assert_same(ip, expected)
+
+
+@pytest.mark.parametrize("E", [4, 8, 16])
+def test_unaligned_views_take_fallback_and_match(cuda, E):
+    b = 15
+    n = 1 << b
+    host = rand_bits(n + 1, E, seed=5000 + E)
+    base = torch.from_numpy(host).to(cuda)
+    view = base[1:]  # 16-byte misaligned for E < 16... and aligned for E=16
+    out = torch.empty(n + 1, dtype=base.dtype, device=cuda)[1:]
+    br.cobra_out_of_place(view, out, br.CobraConfig(4), b)
+    torch.cuda.synchronize()
+    assert_same(out, orc.oracle_permute(host[1:], b))
+    br.cobra_in_place(view, br.CobraConfig(4), b)
+    torch.cuda.synchronize()
+    assert_same(view, orc.oracle_permute(host[1:], b))
+
+
+def test_strided_view(cuda):
+    b = 12
+    host = rand_bits(2 << b, 8, seed=77)
+    base = torch.from_numpy(host).to(cuda)
+    view = base[::2]
+    expected = orc.oracle_permute(host[::2], b)
+    br.xor_permute(view, b)
+    torch.cuda.synchronize()
+    assert_same(view, expected)
+    assert_same(base[1::2], host[1::2])
+
+
+def test_host_arrays_staged_through_device(cuda):
+    """numpy callers of the reference API get the device path, synchronously."""
+    b = 18
+    host = rand_bits(1 << b, 16, seed=9)
+    dest = np.empty_like(host)
+    br.cobra_out_of_place(host, dest, br.CobraConfig(6), b)
+    assert_same(dest, orc.oracle_permute(host, b))
+    a = host.copy()
+    br.recursive_permute(a, b)
+    assert_same(a, orc.oracle_permute(host, b))
+
+
+@pytest.mark.parametrize("b", [1, 2, 6, 11, 16, 19])
+def test_involution(cuda, b):
+    host = rand_bits(1 << b, 8, seed=b)
+    a = torch.from_numpy(host).to(cuda)
+    br.cobra_in_place(a, br.CobraConfig(0), b)
+    br.cobra_in_place(a, br.CobraConfig(0), b)
+    torch.cuda.synchronize()
+    assert_same(a, host)
+
+
+def test_canonical_vector_every_method(cuda):
+    for m in br.METHOD_IDS:
+        a = torch.arange(8, dtype=torch.int64, device=cuda)
+        out = br.make_method(m)(a, 3)
+        got = (a if out is None else out).tolist()
+        assert got == [0, 4, 2, 6, 1, 5, 3, 7], m
+
+
+def test_launch_counter_moves(cuda):
+    before = br.launch_count()
+    a = torch.arange(1 << 20, dtype=torch.float32, device=cuda)
+    br.cobra_in_place(a, br.CobraConfig(6), 20)
+    torch.cuda.synchronize()
+    assert br.launch_count() == before + 1
