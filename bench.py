@@ -1,0 +1,472 @@
+#!/usr/bin/env python
+"""Benchmark: effective HBM GB/s (2*n*elem_bytes / time) of the bit-reversed
+permutation on B200, plus the reference's CPU path timed on the host cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+                    [--impl ours|reference]
+
+A "step" is one permutation of one batch of synthetic input (BASELINE.json
+configs; default cfg2 = the in-place tile-pair swap of n=2^26 float64, the
+configuration the headline metric is quoted on).  Timing: W untimed warm-up
+steps, then EXACTLY K steps, each bracketed by CUDA events on the stream the
+kernel is launched on, with a barrier + device synchronise on both sides; the
+per-rank time is the sum of the K step durations and the job time is the max
+over ranks.  Workloads whose working set is below 4x the L2 get an L2 flush
+(a 512 MiB write) before every step, outside the step's events.
+
+Under torchrun (N > 1) every rank runs its own replica of the single-array
+workloads (cfg1-cfg3: the in-place path does not shard, "replicas only"),
+cfg4 shards the batch rows (no collective), and cfg5 runs the top-bit sharded
+plan with an NCCL all-to-all.  Rank 0 prints ONE JSON line.
+
+--impl reference times the reference's own CPU algorithm for the path (the C
+restatement in oracle/, parallel semi-recursive on all host threads; the
+reference itself is Python+numba and cannot travel to the GPU box) on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (b, torch dtype name, elem bytes, in-place, batch, description)
+    "cfg1": (20, "complex128", 16, False, 1,
+             "out-of-place bit reversal, n=2^20 complex128 (parity target: recursive_permute)"),
+    "cfg2": (26, "float64", 8, True, 1,
+             "in-place bit reversal (tile-pair swap), n=2^26 float64"),
+    "cfg3-4": (30, "float32", 4, False, 1, "out-of-place bit reversal, n=2^30 float32"),
+    "cfg3-8": (30, "float64", 8, False, 1, "out-of-place bit reversal, n=2^30 float64"),
+    "cfg3-16": (30, "complex128", 16, False, 1, "out-of-place bit reversal, n=2^30 complex128"),
+    "cfg4": (16, "complex64", 8, False, 4096,
+             "batched out-of-place bit reversal, 4096 x n=2^16 complex64 (FFT pre-pass)"),
+    "cfg5": (32, "complex64", 8, False, 1,
+             "n=2^32 complex64 sharded by top bits, local reversal + NCCL all-to-all + interleave"),
+}
+METRIC = "effective HBM GB/s (2*n*elem_bytes/time)"
+L2_BYTES = 126 * 10**6
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-soak", action="store_true",
+                    help="skip the 0.5 s clock soak (for profiler runs)")
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0,
+                    help="target seconds of CPU work for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+
+def load_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        v = float(json.loads(p.read_text())["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(workload):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture summary (profiles/traffic.json), or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text())[workload]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms in the background."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.marks = {}
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.monotonic(), line.strip()))
+
+    def mark(self, name):
+        self.marks[name] = time.monotonic()
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        def parse(rows):
+            out = []
+            for _, line in rows:
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    out.append((float(f[0]), float(f[1]), f))
+                except ValueError:
+                    continue
+            return out
+
+        window = "timed"
+        rows = parse([r for r in self.rows if t0 <= r[0] <= t1])
+        if len(rows) < 3:  # timed region shorter than the sampling period
+            window = "warmup+timed+soak"
+            rows = parse([r for r in self.rows
+                          if self.marks.get("load0", t0) <= r[0] <= self.marks.get("load1", t1)])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for _, _, f in rows:
+            for k, name in enumerate(names):
+                if f[4 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": sorted(reasons),
+                "samples": len(rows), "window": window}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU)
+
+
+def cpu_reference_step_fn(workload, threads):
+    """Return (step(), bytes_per_step, sample description, kind) running the
+    reference's CPU algorithm (C restatement, oracle/) on a host array."""
+    from oracle import oracle as orc
+
+    b, dtname, E, inplace, batch, _ = WORKLOADS[workload]
+    np_dt = {"float32": np.float32, "float64": np.float64, "complex64": np.complex64,
+             "complex128": np.complex128}[dtname]
+    rng = np.random.default_rng(0)
+    if workload == "cfg4":
+        # the reference has no batched API: rows over the threads;
+        # each step permutes a bounded block of rows
+        rows = max(threads, 64)
+        arr = rng.standard_normal((rows, 1 << b)).astype(np_dt)
+
+        def step():
+            import concurrent.futures as cf
+
+            with cf.ThreadPoolExecutor(threads) as ex:
+                list(ex.map(lambda r: orc.c_cobra_inplace(arr[r], b, 6), range(rows)))
+
+        return step, 2 * rows * (1 << b) * E, f"{rows} of the 4096 rows per step", "port"
+    if workload == "cfg5":
+        b = 28  # bounded sample: 2^28 of the 2^32 elements per step
+    n = 1 << b
+    arr = rng.standard_normal(n).astype(np_dt) if np_dt in (np.float32, np.float64) else \
+        (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(np_dt)
+
+    def step():
+        orc.c_parallel_semi_recursive(arr, b, threads)
+
+    sample = f"full n=2^{b} array per step" if workload != "cfg5" else \
+        "n=2^28 of the 2^32-element array per step"
+    return step, 2 * n * E, sample, "port"
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+
+    orc.build()
+    threads = os.cpu_count() or 1
+    step, nbytes, sample, kind = cpu_reference_step_fn(args.workload, threads)
+    for _ in range(args.warmup):
+        step()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    value = nbytes * len(ts) / total / 1e9
+    b, dtname, E, inplace, batch, desc = WORKLOADS[args.workload]
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(ts) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": short_dtype(dtname),
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.workload}: {desc}", "b": b, "elem_bytes": E,
+                   "inplace": inplace, "batch": batch},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": sample,
+                         "method": "parallel_semi_recursive_permute (C port of src/parallel.py)"
+                         if args.workload != "cfg4" else "cobra_in_place per row on a thread pool"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def short_dtype(name):
+    return {"float32": "f32", "float64": "f64", "complex64": "c64", "complex128": "c128"}[name]
+
+
+def cpu_baseline(workload, target_s):
+    """The C port timed on the host cores, bounded to ~target_s of CPU work."""
+    threads = os.cpu_count() or 1
+    step, nbytes, sample, kind = cpu_reference_step_fn(workload, threads)
+    step()  # warm (page faults, thread start-up)
+    ts = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > target_s / threads or len(ts) >= 50:
+            break
+    total = sum(ts)
+    return {"value": nbytes * len(ts) / total / 1e9, "unit": "GB/s", "cores": threads,
+            "kind": kind, "sample": f"{sample}, {len(ts)} steps",
+            "method": "parallel_semi_recursive_permute (C port of src/parallel.py:95-156)"
+            if workload != "cfg4" else "cobra_in_place per row on a thread pool"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1708_01873_b200 as br
+    from paper_1708_01873_b200 import _core, _lib, sharded
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    b, dtname, E, inplace, batch, desc = WORKLOADS[args.workload]
+    dtype = getattr(torch, dtname)
+
+    # per-rank work
+    if args.workload == "cfg4":
+        rows = batch // world
+        scaling = "strong"
+        shape = (rows, 1 << b)
+    elif args.workload == "cfg5":
+        if world < 2:
+            sys.stderr.write("cfg5 needs --gpus >= 2 (torchrun)\n")
+            return 2
+        g = sharded.check_plan(b, world)
+        shape = (1 << (b - g),)
+        scaling = "strong"
+    else:
+        shape = (1 << b,)
+        scaling = "weak"
+    n_local = int(np.prod(shape))
+    bytes_local = 2 * n_local * E
+
+    x = torch.empty(n_local * E, dtype=torch.uint8, device=dev).random_(0, 256).view(dtype)
+    x = x.view(shape)
+    y = None if inplace else torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+
+    if args.workload == "cfg5":
+        def step():
+            return sharded.sharded_bitrev(x, b)
+    elif inplace:
+        def step():
+            _core.launch_inplace(x, b)
+    else:
+        def step():
+            _core.launch_oop(x, y, b)
+
+    need_flush = 2 * bytes_local < 4 * L2_BYTES and args.workload != "cfg5"
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if need_flush else None
+
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    sampler.mark("load0")
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    # clock soak: keep the GPU busy ~0.5 s so the sampler sees load clocks
+    t_soak = time.monotonic()
+    while not args.no_soak and time.monotonic() - t_soak < 0.5:
+        for _ in range(8):
+            if flush is not None:
+                flush.zero_()
+            step()
+        torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    t_wall0 = time.monotonic()
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        starts[k].record(stream)
+        step()
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.monotonic()
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    step_s = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
+    rank_time = sum(step_s)
+    if world > 1:
+        t = torch.tensor([rank_time], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        job_time = float(t.item())
+    else:
+        job_time = rank_time
+    sampler.mark("load1")
+
+    # end-to-end through the public API with host buffers (rank 0's replica)
+    e2e = None
+    if not args.no_e2e and args.workload != "cfg5":
+        host = x.cpu().pin_memory()
+        hout = None if inplace else torch.empty_like(host).pin_memory()
+        cfg = br.CobraConfig(6)
+
+        def e2e_step():
+            if args.workload == "cfg4":
+                br.bitrev_batched(host, b, hout)
+            elif inplace:
+                br.cobra_in_place(host, cfg, b)
+            else:
+                br.cobra_out_of_place(host, hout, cfg, b)
+
+        for _ in range(2):
+            e2e_step()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, min(args.steps, 10))
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(reps):
+            e2e_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        t_e2e = ev0.elapsed_time(ev1) / 1e3 / reps
+        e2e = {"value": bytes_local / t_e2e / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": n_local * E, "d2h_bytes_per_step": n_local * E,
+               "ms_per_step": t_e2e * 1e3, "path": "public API on pinned host tensors "
+               "(bitrev_*_host: H2D + kernel + D2H + sync)"}
+    sampler.stop()
+    clocks = sampler.summary(t_wall0, t_wall1)
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    peak, peak_src = load_peak()
+    avg_launch = statistics.mean(step_s)
+    achieved = bytes_local / avg_launch / 1e9
+    value = world * bytes_local * args.steps / job_time / 1e9
+    if args.workload == "cfg5":
+        value = (1 << b) * 2 * E * args.steps / job_time / 1e9
+    traffic = load_traffic(args.workload)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": job_time / args.steps * 1e3,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": short_dtype(dtname), "data": "synthetic (random bit patterns, device-generated)",
+        "config": {
+            "workload": f"{args.workload}: {desc}", "b": b, "elem_bytes": E, "inplace": inplace,
+            "batch": batch, "per_gpu_bytes_moved": bytes_local,
+            "parallelism": {"cfg4": f"batch rows sharded over {world} GPUs",
+                            "cfg5": f"top {world.bit_length() - 1} index bits over {world} GPUs"
+                            }.get(args.workload, f"replicas only ({world} independent arrays)"),
+            "l2": "L2 flushed (512 MiB write) before every step" if need_flush else
+                  f"working set {bytes_local // 2 >> 20} MiB per side > L2, no flush",
+            "tile_bits": _lib.get_tile_bits(E, inplace),
+        },
+        "gelem_per_s": value / (2 * E),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "bitrev_inplace_tile_kernel" if inplace else "bitrev_oop_tile_kernel",
+                     "algorithmic_bytes_per_launch": bytes_local, "peak_source": peak_src,
+                     "frac_of_8TBs_spec": achieved / 8000.0},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "step_ms": {"median": statistics.median(step_s) * 1e3, "min": min(step_s) * 1e3,
+                    "max": max(step_s) * 1e3},
+    }
+    if args.workload == "cfg5":
+        line["roofline"]["kernel"] = "local bitrev + NCCL all-to-all + unpack"
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.workload, args.cpu_sample_s)
+        except Exception as e:  # keep the GPU line even if the host port fails
+            line["cpu_baseline"] = {"value": None, "error": repr(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

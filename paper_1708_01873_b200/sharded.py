@@ -1,0 +1,103 @@
+"""One 2^b array sharded by its top g index bits over G = 2^g ranks.
+
+No reference counterpart (the reference is single-host); this
+is BASELINE config 5.  Rank r owns global indices r*2^(b-g) + j.  Writing
+j = m*G + l (l = low g bits), rev_b(r*2^(b-g) + j) = rev_{b-g}(j)*G + rev_g(r)
+and rev_{b-g}(j) = rev_g(l)*2^(b-2g) + rev_{b-2g}(m), so:
+
+  1. local:  L = bitrev_{b-g}(shard)            -- the single-GPU tile kernel;
+             L is already G contiguous chunks of C = 2^(b-2g) elements,
+             chunk d destined for rank d = rev_g(l);
+  2. exchange: all-to-all with equal chunks      -- NCCL over NVLink/NVSwitch;
+             rank d receives recv[r] = L_r[d];
+  3. local:  out[k*G + rev_g(r)] = recv[r][k]    -- bitrev_sharded_unpack.
+
+Requires b >= 2g.  Each element crosses HBM twice per local step and NVLink
+once (unless it stays on its own rank: 1/G of the data).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from . import _core, _lib
+from .bits import check_width
+
+
+def shard_bits(world_size: int) -> int:
+    g = world_size.bit_length() - 1
+    if world_size < 1 or (1 << g) != world_size:
+        raise ValueError(f"world size must be a power of two, got {world_size}")
+    return g
+
+
+def check_plan(b: int, world_size: int) -> int:
+    check_width(b)
+    g = shard_bits(world_size)
+    if 2 * g > b:
+        raise ValueError(f"sharded bit reversal needs b >= 2*log2(G): b={b}, G={world_size}")
+    return g
+
+
+def _local_bitrev(shard: torch.Tensor, b_local: int) -> torch.Tensor:
+    out = torch.empty_like(shard)
+    _core.launch_oop(shard, out, b_local)
+    return out
+
+
+def _unpack(recv: torch.Tensor, b_local: int, g: int) -> torch.Tensor:
+    out = torch.empty_like(recv)
+    with torch.cuda.device(recv.device):
+        _lib.call("bitrev_sharded_unpack", recv.data_ptr(), out.data_ptr(), b_local, g,
+                  _core.elem_bytes(recv), _core._stream_ptr(recv.device))
+    return out
+
+
+def _all_to_all(recv: torch.Tensor, send: torch.Tensor, group) -> None:
+    dist.all_to_all_single(recv, send, group=group)
+
+
+def sharded_bitrev(local: torch.Tensor, b: int, group=None, *,
+                   local_permute: Callable | None = None,
+                   unpack: Callable | None = None,
+                   all_to_all: Callable | None = None) -> torch.Tensor:
+    """Bit-reverse the global 2^b array whose rank-r shard is `local`.
+
+    Returns this rank's shard of the permuted array (a new tensor).  The three
+    step callables default to the CUDA kernels and NCCL; they are injectable
+    so the exchange logic can be exercised with gloo on CPU tensors in tests.
+    """
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    g = check_plan(b, world)
+    b_local = b - g
+    if local.dim() != 1 or local.shape[0] != (1 << b_local):
+        raise ValueError(f"local shard length {local.shape[0]} does not match 2**{b_local}")
+    local_permute = local_permute or _local_bitrev
+    unpack = unpack or _unpack
+    all_to_all = all_to_all or _all_to_all
+    staged = local_permute(local.contiguous(), b_local)
+    if world == 1:
+        return staged
+    recv = torch.empty_like(staged)
+    all_to_all(recv, staged, group)
+    return unpack(recv, b_local, g)
+
+
+def emulate_sharded(global_array: torch.Tensor, b: int, world_size: int) -> list[torch.Tensor]:
+    """Run the three steps for `world_size` virtual ranks on ONE device, with
+    the exchange done by device copies.  Used to check the plan's kernels on a
+    single GPU; the real exchange is sharded_bitrev under torchrun."""
+    g = check_plan(b, world_size)
+    b_local = b - g
+    S = 1 << b_local
+    C = 1 << (b_local - g)
+    staged = [_local_bitrev(global_array[r * S:(r + 1) * S].contiguous(), b_local)
+              for r in range(world_size)]
+    outs = []
+    for d in range(world_size):
+        recv = torch.cat([staged[r][d * C:(d + 1) * C] for r in range(world_size)])
+        outs.append(_unpack(recv, b_local, g))
+    return outs

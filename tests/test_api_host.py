@@ -1,0 +1,189 @@
+"""Host-side behaviour of the reference-shaped API (no GPU needed): argument
+validation with the reference's messages (tests/test_permutations.py:104-154,
+tests/test_recursive.py:72-117 in the reference), the work-plan helpers of
+src/parallel.py, recursion-plan traces, schedules, and the loud failure when no
+CUDA device is present (there is no CPU path)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1708_01873_b200 as br
+from paper_1708_01873_b200 import recursive as rec
+
+
+# --- validation -----------------------------------------------------------
+
+
+@pytest.mark.parametrize("b", [0, 49, -1])
+def test_width_domain(b):
+    with pytest.raises(ValueError, match="bit width"):
+        br.naive_bitwise_permute(np.zeros(4), b)
+    with pytest.raises(ValueError, match="bit width"):
+        br.check_width(b)
+
+
+def test_length_and_ndim_messages():
+    with pytest.raises(ValueError, match="does not match 2\\*\\*3"):
+        br.xor_permute(np.zeros(9), 3)
+    with pytest.raises(ValueError, match="must be 1-D"):
+        br.cobra_in_place(np.zeros((2, 4)), br.CobraConfig(1), 3)
+    with pytest.raises(ValueError, match="source length"):
+        br.cobra_out_of_place(np.zeros(7), np.zeros(8), br.CobraConfig(1), 3)
+    with pytest.raises(ValueError, match="dest length"):
+        br.cobra_out_of_place(np.zeros(8), np.zeros(7), br.CobraConfig(1), 3)
+    with pytest.raises(ValueError, match="does not match 2\\*\\*4"):
+        br.recursive_permute(np.zeros(8), 4)
+
+
+def test_cobra_config_checks():
+    with pytest.raises(ValueError, match="q must be >= 0"):
+        br.CobraConfig(-1)
+    with pytest.raises(ValueError, match="2q <= b"):
+        br.cobra_in_place(np.zeros(8), br.CobraConfig(2), 3)
+    assert br.default_cobra_q(20) == 6 and br.default_cobra_q(5) == 2
+    assert br.CobraConfig(3).buffer_size == 64
+
+
+def test_overlap_rejected():
+    a = np.zeros(16)
+    with pytest.raises(ValueError, match="overlap"):
+        br.cobra_out_of_place(a, a, br.CobraConfig(1), 4)
+    t = torch.zeros(32)
+    with pytest.raises(ValueError, match="overlap"):
+        br.cobra_out_of_place(t[:16], t[8:24], br.CobraConfig(1), 4)
+
+
+def test_scratch_rules():
+    with pytest.raises(ValueError, match="scratch"):
+        br.stockham_permute(np.zeros(16), 4, scratch=np.zeros(8))
+    with pytest.raises(ValueError, match="scratch"):
+        br.stockham_permute(np.zeros(16), 4, scratch=np.zeros(16, dtype=np.float32))
+    with pytest.raises(ValueError, match="scratch"):
+        br.recursive_permute(np.zeros(1 << 11), 11, br.RecursionPolicy(4), scratch=np.zeros(100))
+    with pytest.raises(ValueError, match="dtype"):
+        br.recursive_permute(np.zeros(1 << 11), 11, br.RecursionPolicy(4),
+                             scratch=np.zeros(1 << 10, dtype=np.int32))
+    with pytest.raises(ValueError, match="scratch"):
+        br.even_odd_permute(np.zeros(16), 4, scratch=np.zeros(3))
+    with pytest.raises(ValueError, match="scratch"):
+        br.parallel_semi_recursive_permute(np.zeros(1 << 11), 11, scratch=np.zeros(10))
+
+
+def test_policy_and_parallel_config_validation():
+    with pytest.raises(ValueError):
+        br.RecursionPolicy(0)
+    with pytest.raises(ValueError):
+        br.RecursionPolicy(4, depth_limit=0)
+    with pytest.raises(ValueError):
+        br.ParallelConfig(threads=-1)
+    with pytest.raises(ValueError):
+        br.ParallelConfig(depth_limit=2)
+
+
+def test_transpose_validation():
+    with pytest.raises(ValueError, match="h must be"):
+        br.transpose_square_inplace(np.zeros(4), -1)
+    with pytest.raises(ValueError, match="4\\*\\*2"):
+        br.transpose_square_inplace(np.zeros(15), 2)
+    br.transpose_square_inplace(np.zeros(1), 0)  # h = 0 is a no-op
+
+
+def test_unknown_method():
+    with pytest.raises(ValueError, match="unknown method"):
+        br.make_method("nope")
+    assert len(br.METHOD_IDS) == 11
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback():
+    with pytest.raises(RuntimeError, match="CUDA"):
+        br.cobra_in_place(np.arange(16.0), br.CobraConfig(1), 4)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        br.cobra_out_of_place(torch.arange(16.0), torch.empty(16), br.CobraConfig(1), 4)
+
+
+# --- work-plan helpers (reference tests/test_parallel.py) ------------------
+
+
+@pytest.mark.parametrize("count,workers", [(1, 1), (7, 3), (64, 8), (100, 7), (5, 9)])
+def test_chunk_ranges_partition(count, workers):
+    chunks = br.chunk_ranges(count, workers)
+    covered = [i for lo, hi in chunks for i in range(lo, hi)]
+    assert covered == list(range(count))
+    assert len(chunks) <= workers
+
+
+@pytest.mark.parametrize("h", [2, 3, 4, 6, 9])
+def test_transpose_tiles_own_each_cell_once(h):
+    side = 1 << h
+    owner = np.zeros((side, side), dtype=int)
+    for kind, r0, c0, size in br.transpose_tiles(h):
+        owner[r0:r0 + size, c0:c0 + size] += 1
+        if kind == "offdiag":
+            owner[c0:c0 + size, r0:r0 + size] += 1
+    assert (owner == 1).all()
+
+
+def test_resolve_threads_env(monkeypatch):
+    monkeypatch.setenv("BITREV_THREADS", "3")
+    assert br.resolve_threads() == 3
+    assert br.resolve_threads(5) == 5
+    monkeypatch.setenv("BITREV_THREADS", "0")
+    with pytest.raises(ValueError):
+        br.resolve_threads()
+
+
+# --- recursion plan (reference tests/test_recursive.py:164-197) -----------
+
+
+def test_trace_structure_even():
+    trace = []
+    rec._plan(0, 12, 0, br.RecursionPolicy(6), trace)
+    kinds = [k for k, _, _ in trace]
+    assert kinds.count("transpose") == 1
+    assert kinds.count("base") == 2 * (1 << 6)
+    t = kinds.index("transpose")
+    assert t == 1 << 6
+
+
+def test_trace_one_even_odd_per_odd_level():
+    trace = []
+    rec._plan(0, 11, 0, br.RecursionPolicy(4), trace)
+    assert trace[0] == ("even_odd", 0, 11)
+    assert sum(1 for k, _, w in trace if k == "even_odd" and w == 11) == 1
+
+
+def test_first_odd_width():
+    assert rec._first_odd_width(20, br.RecursionPolicy(9)) is None
+    assert rec._first_odd_width(11, br.RecursionPolicy(4)) == 11
+    assert rec._first_odd_width(26, br.RecursionPolicy(9)) == 13
+    assert rec._first_odd_width(26, br.RecursionPolicy(9, 1)) is None
+
+
+# --- schedules --------------------------------------------------------------
+
+
+def test_swap_count_law():
+    for b in range(1, 27):
+        assert br.swap_count(b) == ((1 << b) - (1 << ((b + 1) // 2))) // 2
+    assert len(br.cached_schedule(10)) == br.swap_count(10)
+    with pytest.raises(ValueError):
+        br.SwapSchedule(3, np.zeros((3, 3)))
+
+
+def test_rev_naive_semantics():
+    assert br.rev_naive(1, 3) == 4
+    assert br.rev_naive(0b0110, 4) == 6
+    assert [br.rev_naive(i, 3) for i in range(8)] == [0, 4, 2, 6, 1, 5, 3, 7]
+    assert br.BYTE_TABLE[1] == 128 and br.BYTE_TABLE[255] == 255
+    with pytest.raises(ValueError):
+        br.rev_naive(8, 3)
+
+
+def test_csv_round_trip(tmp_path):
+    recs = [br.make_record("cobra", b, r, 1e-6 * (b + r) / 3) for b in (8, 9) for r in range(3)]
+    p = tmp_path / "x.csv"
+    br.write_csv(recs, p)
+    assert br.read_csv(p) == recs
+    assert p.read_text().splitlines()[0] == "method,b,n,replicate,elapsed_s,per_element_s"
