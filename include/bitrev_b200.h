@@ -83,8 +83,9 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
  * Host-buffer variants: H2D copy into caller-provided device scratch, the
  * kernel, D2H copy back, then stream synchronisation.  host_* may be pageable
  * or pinned (pinned is faster).  dev_src/dev_dst (oop) and dev_buf (in-place)
- * must each hold batch * 2^b elements.  This is the call a numpy-array caller
- * of the reference API lands on (same functions as above).
+ * must each hold batch * 2^b elements, or be NULL: the library then takes
+ * stream-ordered scratch (cudaMallocAsync) and frees it before returning.
+ * This is the call a numpy-array caller of the reference API lands on.
  */
 int bitrev_oop_host(const void* host_src, void* host_dst, int b, int elem_bytes, int64_t batch,
                     void* dev_src, void* dev_dst, void* stream);
@@ -135,6 +136,28 @@ int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int e
  */
 int bitrev_get_tile_bits(int elem_bytes, int inplace);
 int bitrev_set_tile_bits(int elem_bytes, int inplace, int q);
+
+/*
+ * Staging path of the shared-memory kernels for (element size, family):
+ * 0 = register staging (LDG.128 -> registers -> STS), 1 = TMA bulk ring
+ * (cp.async.bulk row copies into a multi-stage shared-memory ring completing
+ * on mbarriers).  Output never depends on it; a (q, path) pair that is not
+ * instantiated falls back to path 0.  Initial value from the environment
+ * (BITREV_B200_PATH_OOP / BITREV_B200_PATH_IP), else the measured default.
+ */
+int bitrev_get_tile_path(int elem_bytes, int inplace);
+int bitrev_set_tile_path(int elem_bytes, int inplace, int path);
+
+/*
+ * Tile visit order of the shared-memory kernels: 0 = middle value y equals
+ * the work index; 1 = bit-interleaved (consecutive work items vary y's low
+ * and high bits alternately, giving both the y and the rev(y) side contiguous
+ * DRAM runs); 0x100 | L << 4 | H = y's L low bits vary fastest, then its H
+ * top bits.  Output never depends on it.  Initial value from the environment
+ * (BITREV_B200_ORDER_OOP / BITREV_B200_ORDER_IP), else the measured default.
+ */
+int bitrev_get_tile_order(int inplace);
+int bitrev_set_tile_order(int inplace, int order);
 
 /* Number of kernels this library has launched in this process (all devices). */
 int64_t bitrev_launch_count(void);

@@ -8,6 +8,7 @@ permutation entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -32,6 +33,10 @@ SIGNATURES = {
     "bitrev_sharded_unpack": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _vp]),
     "bitrev_get_tile_bits": (_c_int, [_c_int, _c_int]),
     "bitrev_set_tile_bits": (_c_int, [_c_int, _c_int, _c_int]),
+    "bitrev_get_tile_path": (_c_int, [_c_int, _c_int]),
+    "bitrev_set_tile_path": (_c_int, [_c_int, _c_int, _c_int]),
+    "bitrev_get_tile_order": (_c_int, [_c_int]),
+    "bitrev_set_tile_order": (_c_int, [_c_int, _c_int]),
     "bitrev_launch_count": (_c_i64, []),
 }
 
@@ -53,7 +58,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path is not None else LIB_PATH
+        # BITREV_B200_LIB: load an alternative build (tuning A/B runs only)
+        p = Path(path) if path is not None else Path(os.environ.get("BITREV_B200_LIB", LIB_PATH))
         if not p.exists():
             raise RuntimeError(
                 f"{p} is missing: build it with `python -m paper_1708_01873_b200.build` "
@@ -87,6 +93,22 @@ def version() -> str:
 
 def get_tile_bits(elem_bytes: int, inplace: bool) -> int:
     return int(load().bitrev_get_tile_bits(elem_bytes, int(inplace)))
+
+
+def get_tile_path(elem_bytes: int, inplace: bool) -> int:
+    return int(load().bitrev_get_tile_path(elem_bytes, int(inplace)))
+
+
+def set_tile_path(elem_bytes: int, inplace: bool, path: int) -> None:
+    call("bitrev_set_tile_path", elem_bytes, int(inplace), path)
+
+
+def get_tile_order(inplace: bool) -> int:
+    return int(load().bitrev_get_tile_order(int(inplace)))
+
+
+def set_tile_order(inplace: bool, order: int) -> None:
+    call("bitrev_set_tile_order", int(inplace), order)
 
 
 def set_tile_bits(elem_bytes: int, inplace: bool, q: int) -> None:

@@ -44,24 +44,33 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > built for p in DEPENDS)
 
 
-def build_library(force: bool = False, verbose: bool = False) -> Path:
-    """Compile the CUDA sources into LIB_PATH (skipped when up to date)."""
-    if not force and not needs_build():
+def build_library(force: bool = False, verbose: bool = False, out: Path | None = None,
+                  defines: tuple[str, ...] = ()) -> Path:
+    """Compile the CUDA sources into LIB_PATH (skipped when up to date).
+
+    out/defines build a tuning variant elsewhere (e.g. -DBITREV_MINB_IP=6)."""
+    target = Path(out) if out is not None else LIB_PATH
+    if out is None and not force and not needs_build():
         return LIB_PATH
-    tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-Xptxas", "-v",
-           "-o", str(tmp), *map(str, SOURCES)]
+    tmp = target.with_suffix(".so.tmp")
+    cmd = [_nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in defines), f"-I{INCLUDE}", f"-I{CSRC}",
+           "-Xptxas", "-v", "-o", str(tmp), *map(str, SOURCES)]
     proc = subprocess.run(cmd, capture_output=True, text=True)
-    log = PKG_DIR / "csrc" / "ptxas.log"
+    log = PKG_DIR / "csrc" / ("ptxas.log" if out is None else f"ptxas.{target.stem}.log")
     log.write_text(proc.stdout + proc.stderr)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
         raise RuntimeError(f"nvcc failed ({proc.returncode}): {' '.join(cmd)}")
-    os.replace(tmp, LIB_PATH)
+    os.replace(tmp, target)
     if verbose:
-        print(f"built {LIB_PATH}")
-    return LIB_PATH
+        print(f"built {target}")
+    return target
 
 
 if __name__ == "__main__":
-    build_library(force="--force" in sys.argv, verbose=True)
+    args = sys.argv[1:]
+    out = None
+    defines = tuple(a[2:] for a in args if a.startswith("-D"))
+    if "--out" in args:
+        out = Path(args[args.index("--out") + 1])
+    build_library(force="--force" in args, verbose=True, out=out, defines=defines)

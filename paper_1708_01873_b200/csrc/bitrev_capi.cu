@@ -1,9 +1,12 @@
 // bitrev_capi.cu -- extern "C" entry points of libbitrev_sm100a.so (declared in
 // include/bitrev_b200.h): argument checks, kernel selection, launch geometry.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -47,6 +50,48 @@ int current_q(int E, bool inplace) {
   if (E != 4 && E != 8 && E != 16) return 0;
   const int v = inplace ? g_q_ip[E].load() : g_q_oop[E].load();
   return v ? v : default_q(E, inplace);
+}
+
+// Tile visit order (work_to_y in bitrev_kernels.cuh).  Defaults chosen by
+// measurement; BITREV_B200_ORDER_OOP / BITREV_B200_ORDER_IP override them.
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+std::atomic<int> g_order_oop{-1}, g_order_ip{-1};
+
+// Staging path per (element size, family): 0 = register (LDG/STS), 1 = TMA
+// bulk ring (cp.async.bulk + mbarrier).  -1 = not yet read from the
+// environment (BITREV_B200_PATH_OOP / BITREV_B200_PATH_IP), else default.
+std::atomic<int> g_path_oop[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+std::atomic<int> g_path_ip[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+
+int default_path(int E, bool inplace) {
+  (void)E;
+  (void)inplace;
+  return 0;
+}
+
+int tile_path(int E, bool inplace) {
+  if (E != 4 && E != 8 && E != 16) return 0;
+  std::atomic<int>& p = inplace ? g_path_ip[E] : g_path_oop[E];
+  int v = p.load();
+  if (v < 0) {
+    v = env_int(inplace ? "BITREV_B200_PATH_IP" : "BITREV_B200_PATH_OOP", default_path(E, inplace));
+    p.store(v);
+  }
+  return v;
+}
+
+int tile_order(bool inplace) {
+  std::atomic<int>& o = inplace ? g_order_ip : g_order_oop;
+  int v = o.load();
+  if (v < 0) {
+    v = env_int(inplace ? "BITREV_B200_ORDER_IP" : "BITREV_B200_ORDER_OOP", 0);
+    o.store(v);
+  }
+  return v;
 }
 
 struct DevInfo {
@@ -114,7 +159,7 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
   a.ntiles = (uint64_t)batch << a.m;
   a.src_bstride = sbs * E;
   a.dst_bstride = dbs * E;
-  a.y_begin = 0;
+  a.order = tile_order(false);
   const int grid = grid_for(a.ntiles, per_sm);
   kern<<<grid, T::THREADS, T::BYTES, st>>>(a);
   return finish_launch();
@@ -136,10 +181,137 @@ int launch_ip_tile(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st)
   a.ntiles = (uint64_t)batch << a.m;
   a.src_bstride = bs * E;
   a.dst_bstride = bs * E;
-  a.y_begin = 0;
+  a.order = tile_order(true);
   const int grid = grid_for(a.ntiles, per_sm);
   kern<<<grid, T::THREADS, 2 * T::BYTES, st>>>(a);
   return finish_launch();
+}
+
+template <int E, int Q, bool INPLACE>
+int launch_bulk(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+                cudaStream_t st) {
+  using B = Bulk<E, Q, INPLACE>;
+  static_assert(B::SMEM <= 227 * 1024, "bulk ring exceeds shared memory");
+  auto kern = bitrev_bulk_kernel<E, Q, INPLACE>;
+  static int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, B::SMEM);
+    return occupancy(kern, B::THREADS, B::SMEM);
+  }();
+  TileArgs a;
+  a.src = static_cast<const char*>(src);
+  a.dst = static_cast<char*>(dst);
+  a.b = b;
+  a.m = b - 2 * Q;
+  a.ntiles = (uint64_t)batch << a.m;
+  a.src_bstride = sbs * E;
+  a.dst_bstride = dbs * E;
+  a.order = tile_order(INPLACE);
+  const int grid = grid_for(a.ntiles, per_sm);
+  kern<<<grid, B::THREADS, B::SMEM, st>>>(a);
+  return finish_launch();
+}
+
+int dispatch_bulk(int E, int q, bool inplace, const void* src, void* dst, int b, int64_t batch,
+                  int64_t sbs, int64_t dbs, cudaStream_t st) {
+#define BULK(E_, Q_)                                                                   \
+  if (E == E_ && q == Q_) {                                                            \
+    return inplace ? launch_bulk<E_, Q_, true>(src, dst, b, batch, sbs, dbs, st)       \
+                   : launch_bulk<E_, Q_, false>(src, dst, b, batch, sbs, dbs, st);     \
+  }
+  BULK(4, 6) BULK(8, 5) BULK(8, 6) BULK(16, 4) BULK(16, 5)
+#undef BULK
+  if (!inplace) {
+    if (E == 4 && q == 7) return launch_bulk<4, 7, false>(src, dst, b, batch, sbs, dbs, st);
+    if (E == 16 && q == 6) return launch_bulk<16, 6, false>(src, dst, b, batch, sbs, dbs, st);
+  }
+  return BITREV_ETILE;
+}
+
+// ---------------------------------------------------------------------------
+// TMA tensor path
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 5-D view described in bitrev_kernels.cuh (Tma family).  Returns false if
+// the driver rejects it (the caller then takes the register path).
+bool encode_tile_map(CUtensorMap* map, const void* base, int b, int E, int q, int64_t batch,
+                     int64_t bstride_elems) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int unit = E == 4 ? 4 : 8;
+  const uint64_t row = (uint64_t)E << q;
+  const int m = b - 2 * q;
+  if (m > 31 || batch > (int64_t(1) << 31)) return false;
+  cuuint64_t dims[5] = {128u / unit, (cuuint64_t)1 << q, row / 128, (cuuint64_t)1 << m,
+                        (cuuint64_t)batch};
+  cuuint64_t strides[4] = {(cuuint64_t)E << (b - q), 128, row,
+                           (cuuint64_t)(batch > 1 ? bstride_elems : (int64_t(1) << b)) * E};
+  cuuint32_t box[5] = {128u / unit, 1u << q, (cuuint32_t)(row / 128), 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = fn(map, unit == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64,
+                        5, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int E, int Q, bool INPLACE>
+int launch_tma(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+               cudaStream_t st) {
+  using B = Tma<E, Q, INPLACE>;
+  static_assert(B::SMEM <= 227 * 1024, "tma ring exceeds shared memory");
+  CUtensorMap map;
+  if (!encode_tile_map(&map, src, b, E, Q, batch, sbs)) return BITREV_ETILE;
+  auto kern = bitrev_tma_kernel<E, Q, INPLACE>;
+  static int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, B::SMEM);
+    return occupancy(kern, B::THREADS, B::SMEM);
+  }();
+  TileArgs a;
+  a.src = static_cast<const char*>(src);
+  a.dst = static_cast<char*>(dst);
+  a.b = b;
+  a.m = b - 2 * Q;
+  a.ntiles = (uint64_t)batch << a.m;
+  a.src_bstride = sbs * E;
+  a.dst_bstride = dbs * E;
+  a.order = tile_order(INPLACE);
+  const int grid = grid_for(a.ntiles, per_sm);
+  kern<<<grid, B::THREADS, B::SMEM, st>>>(map, a);
+  return finish_launch();
+}
+
+int dispatch_tma(int E, int q, bool inplace, const void* src, void* dst, int b, int64_t batch,
+                 int64_t sbs, int64_t dbs, cudaStream_t st) {
+#define TMA(E_, Q_)                                                                \
+  if (E == E_ && q == Q_) {                                                        \
+    return inplace ? launch_tma<E_, Q_, true>(src, dst, b, batch, sbs, dbs, st)    \
+                   : launch_tma<E_, Q_, false>(src, dst, b, batch, sbs, dbs, st);  \
+  }
+  TMA(4, 5) TMA(4, 6) TMA(8, 4) TMA(8, 5) TMA(8, 6) TMA(16, 3) TMA(16, 4) TMA(16, 5)
+#undef TMA
+  if (!inplace) {
+    if (E == 4 && q == 7) return launch_tma<4, 7, false>(src, dst, b, batch, sbs, dbs, st);
+    if (E == 16 && q == 6) return launch_tma<16, 6, false>(src, dst, b, batch, sbs, dbs, st);
+  }
+  return BITREV_ETILE;
+}
+
+bool bulk_supported(int E, int q, bool inplace) {
+  if ((E == 4 && q == 6) || (E == 8 && (q == 5 || q == 6)) || (E == 16 && (q == 4 || q == 5)))
+    return true;
+  return !inplace && ((E == 4 && q == 7) || (E == 16 && q == 6));
 }
 
 int dispatch_oop_tile(int E, int q, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
@@ -332,8 +504,16 @@ int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
   const int q = pick_q(E, b, false);
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
-  if (q && vec_ok)
+  if (q && vec_ok) {
+    if (tile_path(E, false) == 2) {
+      const int rc2 = dispatch_tma(E, q, false, src, dst, b, batch, src_batch_stride,
+                                   dst_batch_stride, st);
+      if (rc2 != BITREV_ETILE) return rc2;
+    }
+    if (tile_path(E, false) == 1 && bulk_supported(E, q, false))
+      return dispatch_bulk(E, q, false, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
     return dispatch_oop_tile(E, q, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
+  }
   return dispatch_gather(E, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
 }
 
@@ -350,7 +530,15 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
   if (n * E <= kSmallBytes) return dispatch_small(E, a, a, b, batch, batch_stride, batch_stride, st);
   const int q = pick_q(E, b, true);
   const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
-  if (q && vec_ok) return dispatch_ip_tile(E, q, a, b, batch, batch_stride, st);
+  if (q && vec_ok) {
+    if (tile_path(E, true) == 2) {
+      const int rc2 = dispatch_tma(E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
+      if (rc2 != BITREV_ETILE) return rc2;
+    }
+    if (tile_path(E, true) == 1 && bulk_supported(E, q, true))
+      return dispatch_bulk(E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
+    return dispatch_ip_tile(E, q, a, b, batch, batch_stride, st);
+  }
   return dispatch_swap(E, a, b, batch, batch_stride, st);
 }
 
@@ -358,36 +546,62 @@ int bitrev_oop_host(const void* host_src, void* host_dst, int b, int elem_bytes,
                     void* dev_src, void* dev_dst, void* stream) {
   int rc = check_common(b, elem_bytes, batch);
   if (rc) return rc;
-  if (!host_src || !host_dst || !dev_src || !dev_dst) return BITREV_ENULL;
+  if (!host_src || !host_dst) return BITREV_ENULL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
-  cudaError_t e = cudaMemcpyAsync(dev_src, host_src, bytes, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return (int)e;
+  // NULL scratch: stream-ordered allocation from the device's default pool
+  void* own = nullptr;
+  if (!dev_src || !dev_dst) {
+    cudaError_t e = cudaMallocAsync(&own, 2 * bytes, st);
+    if (e != cudaSuccess) return (int)e;
+    dev_src = own;
+    dev_dst = static_cast<char*>(own) + bytes;
+  }
   const int64_t n = int64_t(1) << b;
-  rc = bitrev_oop(dev_src, dev_dst, b, elem_bytes, batch, n, n, stream);
-  if (rc) return rc;
-  e = cudaMemcpyAsync(host_dst, dev_dst, bytes, cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return (int)e;
+  cudaError_t e = cudaMemcpyAsync(dev_src, host_src, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    rc = bitrev_oop(dev_src, dev_dst, b, elem_bytes, batch, n, n, stream);
+    if (rc == BITREV_OK) {
+      e = cudaMemcpyAsync(host_dst, dev_dst, bytes, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) rc = (int)e;
+    }
+  } else {
+    rc = (int)e;
+  }
+  if (own) cudaFreeAsync(own, st);
   e = cudaStreamSynchronize(st);
-  return e == cudaSuccess ? BITREV_OK : (int)e;
+  if (rc == BITREV_OK && e != cudaSuccess) rc = (int)e;
+  return rc;
 }
 
 int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void* dev_buf,
                         void* stream) {
   int rc = check_common(b, elem_bytes, batch);
   if (rc) return rc;
-  if (!host_a || !dev_buf) return BITREV_ENULL;
+  if (!host_a) return BITREV_ENULL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
-  cudaError_t e = cudaMemcpyAsync(dev_buf, host_a, bytes, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return (int)e;
+  void* own = nullptr;
+  if (!dev_buf) {
+    cudaError_t e = cudaMallocAsync(&own, bytes, st);
+    if (e != cudaSuccess) return (int)e;
+    dev_buf = own;
+  }
   const int64_t n = int64_t(1) << b;
-  rc = bitrev_inplace(dev_buf, b, elem_bytes, batch, n, stream);
-  if (rc) return rc;
-  e = cudaMemcpyAsync(host_a, dev_buf, bytes, cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return (int)e;
+  cudaError_t e = cudaMemcpyAsync(dev_buf, host_a, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    rc = bitrev_inplace(dev_buf, b, elem_bytes, batch, n, stream);
+    if (rc == BITREV_OK) {
+      e = cudaMemcpyAsync(host_a, dev_buf, bytes, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) rc = (int)e;
+    }
+  } else {
+    rc = (int)e;
+  }
+  if (own) cudaFreeAsync(own, st);
   e = cudaStreamSynchronize(st);
-  return e == cudaSuccess ? BITREV_OK : (int)e;
+  if (rc == BITREV_OK && e != cudaSuccess) rc = (int)e;
+  return rc;
 }
 
 int bitrev_transpose_square(void* a, int h, int elem_bytes, int64_t batch, int64_t batch_stride,
@@ -499,6 +713,24 @@ int bitrev_set_tile_bits(int elem_bytes, int inplace, int q) {
   if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16) return BITREV_ETILE;
   if (q != 0 && !q_supported(elem_bytes, q)) return BITREV_ETILE;
   (inplace ? g_q_ip : g_q_oop)[elem_bytes].store(q);
+  return BITREV_OK;
+}
+
+int bitrev_get_tile_path(int elem_bytes, int inplace) { return tile_path(elem_bytes, inplace != 0); }
+
+int bitrev_set_tile_path(int elem_bytes, int inplace, int path) {
+  if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16) return BITREV_ETILE;
+  if (path < 0 || path > 2) return BITREV_ETILE;
+  (inplace ? g_path_ip : g_path_oop)[elem_bytes].store(path);
+  return BITREV_OK;
+}
+
+int bitrev_get_tile_order(int inplace) { return tile_order(inplace != 0); }
+
+int bitrev_set_tile_order(int inplace, int order) {
+  if (order < 0 || (order > 1 && (order & ~0x1ff) != 0) || (order > 1 && order < 0x100))
+    return BITREV_ETILE;
+  (inplace ? g_order_ip : g_order_oop).store(order);
   return BITREV_OK;
 }
 

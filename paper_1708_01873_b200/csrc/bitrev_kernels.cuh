@@ -26,7 +26,20 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
+
+// Build-time tuning knobs (defaults are the measured best; tools/variants.sh
+// builds alternatives side by side for A/B runs).
+#ifndef BITREV_IP_NC
+#define BITREV_IP_NC 0  // in-place loads through the non-coherent path
+#endif
+#ifndef BITREV_MINB_OOP
+#define BITREV_MINB_OOP 1  // __launch_bounds__ min CTAs/SM, out-of-place tile kernel
+#endif
+#ifndef BITREV_MINB_IP
+#define BITREV_MINB_IP 1  // __launch_bounds__ min CTAs/SM, in-place tile kernel
+#endif
 
 namespace bitrev_b200 {
 
@@ -191,14 +204,56 @@ struct TileArgs {
   uint64_t ntiles;     // batch << m (oop) or batch << m (in-place, incl. skipped)
   int64_t src_bstride; // bytes between batch rows
   int64_t dst_bstride;
-  uint64_t y_begin;    // first middle value (host-staged chunking); usually 0
+  int order;           // 0: y = work index; 1: bit-interleaved (see work_to_y)
 };
+
+// Gather the even bits of x into its low half (Morton decode).
+__device__ __forceinline__ uint64_t compact_even(uint64_t x) {
+  x &= 0x5555555555555555ull;
+  x = (x | (x >> 1)) & 0x3333333333333333ull;
+  x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x >> 16)) & 0x00000000FFFFFFFFull;
+  return x;
+}
+
+// Middle value y visited at work index w (a bijection of [0, 2^m)).
+// order 0: y = w.  CTAs running together then read adjacent tiles (long
+// contiguous source runs) but write rev(y) tiles scattered over the slab.
+// order 1: w's bits alternate between y's low end and y's high end
+// (w bit 2k -> y bit k, w bit 2k+1 -> y bit m-1-k), so a window of 2^j
+// consecutive work items varies y in its ~j/2 lowest AND ~j/2 highest bits --
+// and rev(y) likewise: both the y side and the rev(y) side of concurrently
+// running CTAs form runs of ~2^(j/2) adjacent tiles.
+__device__ __forceinline__ uint64_t work_to_y(uint64_t w, int m, int order) {
+  if (order == 0 || m < 2) return w;
+  if (order == 1) {
+    const int h = m >> 1;
+    const uint64_t mask = (1ull << h) - 1;
+    uint64_t y = compact_even(w) & mask;
+    y |= dev_rev(compact_even(w >> 1) & mask, h) << (m - h);
+    if (m & 1) y |= ((w >> (2 * h)) & 1ull) << h;
+    return y;
+  }
+  // order = 0x100 | L << 4 | H: the L lowest work bits are y's low bits
+  // (runs of 2^L adjacent tiles on the y side), the next H work bits are y's
+  // top bits (runs of 2^H adjacent tiles on the rev(y) side), the rest fill
+  // the middle.  Clamped so that L + H <= m.
+  int L = (order >> 4) & 15, H = order & 15;
+  if (L > m) L = m;
+  if (H > m - L) H = m - L;
+  const uint64_t lo = w & ((1ull << L) - 1);
+  const uint64_t hi = (w >> L) & ((1ull << H) - 1);
+  const uint64_t mid = w >> (L + H);
+  return (hi << (m - H)) | (mid << L) | lo;
+}
 
 // ---------------------------------------------------------------------------
 // out-of-place tile kernel (replaces _cobra_copy, src/permutations.py:225-249)
 
 template <int E, int Q>
-__global__ void __launch_bounds__(Tile<E, Q>::THREADS)
+__global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_OOP)
     bitrev_oop_tile_kernel(TileArgs a) {
   using T = Tile<E, Q>;
   extern __shared__ __align__(16) uint4 smem[];
@@ -209,12 +264,12 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS)
   uint64_t t = blockIdx.x;
   if (t >= a.ntiles) return;
   auto src_tile = [&](uint64_t tt) {
-    const uint64_t bi = tt >> a.m, y = (tt & mmask) + a.y_begin;
+    const uint64_t bi = tt >> a.m, y = work_to_y(tt & mmask, a.m, a.order);
     return a.src + bi * a.src_bstride + (y << Q) * E;
   };
   tile_load<E, Q, true>(r, src_tile(t), row_stride);
   for (;;) {
-    const uint64_t bi = t >> a.m, y = (t & mmask) + a.y_begin;
+    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
     tile_stage<E, Q>(r, smem);
     __syncthreads();
     const uint64_t tn = t + gridDim.x;
@@ -239,7 +294,7 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS)
 // first write.
 
 template <int E, int Q>
-__global__ void __launch_bounds__(Tile<E, Q>::THREADS)
+__global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
     bitrev_inplace_tile_kernel(TileArgs a) {
   using T = Tile<E, Q>;
   extern __shared__ __align__(16) uint4 smem[];
@@ -252,24 +307,26 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS)
   // next work item at or after tt with y <= rev(y)
   auto advance = [&](uint64_t tt) {
     while (tt < a.ntiles) {
-      const uint64_t y = tt & mmask;
+      const uint64_t y = work_to_y(tt & mmask, a.m, a.order);
       if (dev_rev(y, a.m) >= y) break;
       tt += gridDim.x;
     }
     return tt;
   };
   auto issue = [&](uint64_t tt) {
-    const uint64_t bi = tt >> a.m, y = tt & mmask, ry = dev_rev(y, a.m);
+    const uint64_t bi = tt >> a.m, y = work_to_y(tt & mmask, a.m, a.order),
+                   ry = dev_rev(y, a.m);
     const char* base = a.src + bi * a.src_bstride;
-    tile_load<E, Q, false>(r0, base + (y << Q) * E, row_stride);
-    if (ry != y) tile_load<E, Q, false>(r1, base + (ry << Q) * E, row_stride);
+    tile_load<E, Q, BITREV_IP_NC>(r0, base + (y << Q) * E, row_stride);
+    if (ry != y) tile_load<E, Q, BITREV_IP_NC>(r1, base + (ry << Q) * E, row_stride);
   };
 
   uint64_t t = advance(blockIdx.x);
   if (t >= a.ntiles) return;
   issue(t);
   for (;;) {
-    const uint64_t bi = t >> a.m, y = t & mmask, ry = dev_rev(y, a.m);
+    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order),
+                   ry = dev_rev(y, a.m);
     const bool pair = ry != y;
     tile_stage<E, Q>(r0, U0);
     if (pair) tile_stage<E, Q>(r1, U1);
@@ -282,6 +339,325 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS)
     if (tn >= a.ntiles) break;
     __syncthreads();
     t = tn;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk-copy family: cp.async.bulk row copies into a multi-stage smem ring
+//
+// The register-staged kernels above hold every in-flight byte in registers,
+// which caps the bytes in flight per SM (occupancy is register-limited) and
+// leaves the in-place kernel latency-bound.  Here each tile row (2^Q*E
+// contiguous bytes) is one `cp.async.bulk.shared::cluster.global` copy that
+// completes on a per-stage mbarrier; a CTA keeps NS-1 work items loading
+// while it drains the oldest, so in-flight bytes cost shared memory only.
+//
+// Shared layout per tile: row x at x*PITCH, PITCH = 2^Q*E + 16 (the 16-byte
+// pad rotates consecutive rows across the 8 bank groups).  The drain is the
+// register-staged kernel's transpose moved to the read side: a thread reads
+// the 16-byte chunk c of the V rows g + k*2^Q/V (consecutive lanes take
+// consecutive g: conflict-free LDS.128), transposes V x V in registers, and
+// writes V vectors to destination rows rev_Q(c*V + j) at chunk rev(g) (a warp
+// covers whole contiguous destination rows).
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int E, int Q, bool INPLACE>
+struct Bulk {
+  static constexpr int S = 1 << Q;
+  static constexpr int V = 16 / E;
+  static constexpr int LV = const_log2(V);
+  static constexpr int G = S / V;              // row groups == 16-byte chunks per row
+  static constexpr int ROW = S * E;            // bytes per tile row
+  static constexpr int PITCH = ROW + 16;
+  static constexpr int TILE = S * PITCH;       // smem bytes per staged tile
+  static constexpr int TILES = INPLACE ? 2 : 1;
+  static constexpr int STAGE = TILES * TILE;
+  static constexpr int NS_RAW = 98304 / STAGE;
+  static constexpr int NS = NS_RAW < 2 ? 2 : (NS_RAW > 8 ? 8 : NS_RAW);  // ring depth
+  static constexpr int ITEMS = G * G;          // drain items (V chunks each)
+  static constexpr int THREADS = ITEMS < 256 ? ITEMS : 256;
+  static constexpr int IPT = ITEMS / THREADS;
+  static constexpr int SMEM = NS * STAGE + NS * 8;
+  static_assert(E == 4 || E == 8 || E == 16, "bulk kernels move 4/8/16-byte elements");
+  static_assert(G >= 8 && ROW % 16 == 0, "chunk geometry");
+  static_assert(ITEMS % THREADS == 0 && THREADS >= 32, "even split");
+  static_assert(S <= 32 * 4, "rows per tile issued by one warp");
+};
+
+template <int E, int Q, bool INPLACE>
+__device__ __forceinline__ void bulk_drain(const unsigned char* tile, char* dst_base,
+                                           uint64_t row_stride) {
+  using B = Bulk<E, Q, INPLACE>;
+#pragma unroll
+  for (int it = 0; it < B::IPT; ++it) {
+    const int id = it * B::THREADS + threadIdx.x;
+    const int g = id % B::G;
+    const int c = id / B::G;
+    uint4 v[B::V];
+#pragma unroll
+    for (int k = 0; k < B::V; ++k)
+      v[k] = *reinterpret_cast<const uint4*>(tile + (g + k * B::G) * B::PITCH + c * 16);
+    const uint64_t col = __brev((unsigned)g) >> (32 - (Q - B::LV));
+    char* base = dst_base + col * 16;
+    if constexpr (B::V == 1) {
+      st_vec(base + (uint64_t)(__brev((unsigned)c) >> (32 - Q)) * row_stride, xpose<E, 0>(v));
+    } else if constexpr (B::V == 2) {
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * 2 + 0)) >> (32 - Q)) * row_stride,
+             xpose<E, 0>(v));
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * 2 + 1)) >> (32 - Q)) * row_stride,
+             xpose<E, 1>(v));
+    } else {
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * 4 + 0)) >> (32 - Q)) * row_stride,
+             xpose<E, 0>(v));
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * 4 + 1)) >> (32 - Q)) * row_stride,
+             xpose<E, 1>(v));
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * 4 + 2)) >> (32 - Q)) * row_stride,
+             xpose<E, 2>(v));
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * 4 + 3)) >> (32 - Q)) * row_stride,
+             xpose<E, 3>(v));
+    }
+  }
+}
+
+// Persistent ring kernel.  Out of place: one item = one tile y.  In place: one
+// item = the tile pair {y, rev(y)} with y <= rev(y) (both tiles staged before
+// either is written, as in the register kernel).  Warp 0 is also the producer:
+// at iteration i it refills the slot drained at iteration i-1 (released by the
+// barrier that ends every iteration) with item i+NS-1.
+template <int E, int Q, bool INPLACE>
+__global__ void __launch_bounds__(Bulk<E, Q, INPLACE>::THREADS)
+    bitrev_bulk_kernel(TileArgs a) {
+  using B = Bulk<E, Q, INPLACE>;
+  extern __shared__ __align__(128) unsigned char smem_b[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_b + B::NS * B::STAGE);
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t mmask = (1ull << a.m) - 1;
+
+  auto valid_item = [&](uint64_t tt) {
+    if constexpr (!INPLACE) return true;
+    const uint64_t y = work_to_y(tt & mmask, a.m, a.order);
+    return dev_rev(y, a.m) >= y;
+  };
+  auto advance = [&](uint64_t tt) {
+    while (tt < a.ntiles && !valid_item(tt)) tt += gridDim.x;
+    return tt;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < B::NS; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const bool producer = threadIdx.x < 32;
+  const int lane = threadIdx.x & 31;
+  uint64_t tp = advance(blockIdx.x);  // producer's next item (warp 0 only)
+  auto produce = [&](int slot) {
+    if (tp >= a.ntiles) return;
+    const uint64_t bi = tp >> a.m, y = work_to_y(tp & mmask, a.m, a.order);
+    const uint64_t ry = dev_rev(y, a.m);
+    const bool pair = INPLACE && ry != y;
+    unsigned char* st = smem_b + slot * B::STAGE;
+    const char* base = a.src + bi * a.src_bstride;
+    if (lane == 0) mbar_expect_tx(&bars[slot], (pair ? 2 : 1) * B::S * B::ROW);
+    __syncwarp();
+    for (int x = lane; x < B::S; x += 32) {
+      bulk_g2s(st + x * B::PITCH, base + x * row_stride + (y << Q) * E, B::ROW, &bars[slot]);
+      if (pair)
+        bulk_g2s(st + B::TILE + x * B::PITCH, base + x * row_stride + (ry << Q) * E, B::ROW,
+                 &bars[slot]);
+    }
+    tp = advance(tp + gridDim.x);
+  };
+  if (producer)
+    for (int s = 0; s < B::NS - 1; ++s) produce(s);
+
+  uint64_t t = advance(blockIdx.x);
+  for (int i = 0; t < a.ntiles; ++i) {
+    const int slot = i % B::NS;
+    if (producer) produce((i + B::NS - 1) % B::NS);
+    mbar_wait(&bars[slot], (uint32_t)((i / B::NS) & 1));
+    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
+    const uint64_t ry = dev_rev(y, a.m);
+    const unsigned char* st = smem_b + slot * B::STAGE;
+    char* dbase = a.dst + bi * a.dst_bstride;
+    bulk_drain<E, Q, INPLACE>(st, dbase + (ry << Q) * E, row_stride);
+    if (INPLACE && ry != y) bulk_drain<E, Q, INPLACE>(st + B::TILE, dbase + (y << Q) * E, row_stride);
+    __syncthreads();
+    t = advance(t + gridDim.x);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA tensor family: one cp.async.bulk.tensor per tile
+//
+// The 1-D bulk family needs one copy instruction per tile row, and
+// cp.async.bulk takes uniform operands, so 32 lanes issuing their own rows
+// serialise through an ELECT loop (ncu: the producer warp dominates every
+// iteration).  Here the array is described by a 5-D tensor map
+//     d0: 128-byte unit run   (unit = 4 B for E = 4, else 8 B)
+//     d1: tile row x          stride 2^(b-Q) * E
+//     d2: 128-byte piece      stride 128 B          (2^Q*E / 128 pieces)
+//     d3: middle value y      stride 2^Q * E
+//     d4: batch row           stride batch_stride * E
+// so the box {128/unit, 2^Q, pieces, 1, 1} at (0, 0, 0, y, batch) is exactly
+// tile y, fetched by ONE instruction.  With CU_TENSOR_MAP_SWIZZLE_128B the
+// 16-byte chunk cc of 128-byte segment R = piece * 2^Q + x lands at chunk
+// cc ^ (x & 7): lanes reading consecutive rows x hit 8 distinct bank groups.
+
+template <int E, int Q, bool INPLACE>
+struct Tma {
+  static constexpr int S = 1 << Q;
+  static constexpr int V = 16 / E;
+  static constexpr int LV = const_log2(V);
+  static constexpr int G = S / V;
+  static constexpr int ROW = S * E;
+  static constexpr int P = ROW / 128;          // 128-byte pieces per row
+  static constexpr int TILE = S * ROW;         // dense, 1024-byte aligned
+  static constexpr int TILES = INPLACE ? 2 : 1;
+  static constexpr int STAGE = TILES * TILE;
+  static constexpr int NS_RAW = 98304 / STAGE;
+  static constexpr int NS = NS_RAW < 2 ? 2 : (NS_RAW > 8 ? 8 : NS_RAW);
+  static constexpr int ITEMS = G * G;
+  static constexpr int THREADS = ITEMS < 256 ? ITEMS : 256;
+  static constexpr int IPT = ITEMS / THREADS;
+  static constexpr int SMEM = NS * STAGE + 1024 + NS * 8;  // + alignment slack
+  static_assert(ROW % 128 == 0 && S >= 8, "tensor tiles need 128-byte rows");
+  static_assert(ITEMS % THREADS == 0 && THREADS >= 32, "even split");
+};
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const void* tmap, int c0, int c1, int c2,
+                                            int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int E, int Q, bool INPLACE>
+__device__ __forceinline__ void tma_drain(const unsigned char* tile, char* dst_base,
+                                          uint64_t row_stride) {
+  using B = Tma<E, Q, INPLACE>;
+#pragma unroll
+  for (int it = 0; it < B::IPT; ++it) {
+    const int id = it * B::THREADS + threadIdx.x;
+    const int g = id % B::G;
+    const int c = id / B::G;
+    const int piece = c >> 3, cc = c & 7;
+    uint4 v[B::V];
+#pragma unroll
+    for (int k = 0; k < B::V; ++k) {
+      const int x = g + k * B::G;
+      v[k] = *reinterpret_cast<const uint4*>(tile + (piece * B::S + x) * 128 +
+                                             ((cc ^ (x & 7)) << 4));
+    }
+    const uint64_t col = __brev((unsigned)g) >> (32 - (Q - B::LV));
+    char* base = dst_base + col * 16;
+#pragma unroll
+    for (int j = 0; j < B::V; ++j) {
+      uint4 w;
+      if (j == 0) w = xpose<E, 0>(v);
+      if constexpr (B::V > 1) { if (j == 1) w = xpose<E, 1>(v); }
+      if constexpr (B::V > 2) {
+        if (j == 2) w = xpose<E, 2>(v);
+        if (j == 3) w = xpose<E, 3>(v);
+      }
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * B::V + j)) >> (32 - Q)) * row_stride, w);
+    }
+  }
+}
+
+template <int E, int Q, bool INPLACE>
+__global__ void __launch_bounds__(Tma<E, Q, INPLACE>::THREADS)
+    bitrev_tma_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a) {
+  using B = Tma<E, Q, INPLACE>;
+  extern __shared__ __align__(1024) unsigned char smem_t_raw[];
+  unsigned char* smem_t = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_t_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_t + B::NS * B::STAGE);
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t mmask = (1ull << a.m) - 1;
+
+  auto advance = [&](uint64_t tt) {
+    if constexpr (INPLACE) {
+      while (tt < a.ntiles) {
+        const uint64_t y = work_to_y(tt & mmask, a.m, a.order);
+        if (dev_rev(y, a.m) >= y) break;
+        tt += gridDim.x;
+      }
+    }
+    return tt;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < B::NS; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  uint64_t tp = advance(blockIdx.x);  // producer (thread 0) cursor
+  auto produce = [&](int slot) {
+    if (tp >= a.ntiles) return;
+    const uint64_t y = work_to_y(tp & mmask, a.m, a.order);
+    const int bi = (int)(tp >> a.m);
+    const uint64_t ry = dev_rev(y, a.m);
+    const bool pair = INPLACE && ry != y;
+    unsigned char* st = smem_t + slot * B::STAGE;
+    mbar_expect_tx(&bars[slot], (pair ? 2 : 1) * B::TILE);
+    tma_load_5d(st, &tmap, 0, 0, 0, (int)y, bi, &bars[slot]);
+    if (pair) tma_load_5d(st + B::TILE, &tmap, 0, 0, 0, (int)ry, bi, &bars[slot]);
+    tp = advance(tp + gridDim.x);
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < B::NS - 1; ++s) produce(s);
+
+  uint64_t t = advance(blockIdx.x);
+  for (int i = 0; t < a.ntiles; ++i) {
+    const int slot = i % B::NS;
+    if (threadIdx.x == 0) produce((i + B::NS - 1) % B::NS);
+    mbar_wait(&bars[slot], (uint32_t)((i / B::NS) & 1));
+    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
+    const uint64_t ry = dev_rev(y, a.m);
+    const unsigned char* st = smem_t + slot * B::STAGE;
+    char* dbase = a.dst + bi * a.dst_bstride;
+    tma_drain<E, Q, INPLACE>(st, dbase + (ry << Q) * E, row_stride);
+    if (INPLACE && ry != y) tma_drain<E, Q, INPLACE>(st + B::TILE, dbase + (y << Q) * E, row_stride);
+    __syncthreads();
+    t = advance(t + gridDim.x);
   }
 }
 

@@ -71,6 +71,15 @@ def test_tile_bits_registry():
         _lib.set_tile_bits(2, False, 5)
 
 
+def test_tile_order_registry():
+    old = _lib.get_tile_order(True)
+    _lib.set_tile_order(True, 1)
+    assert _lib.get_tile_order(True) == 1
+    _lib.set_tile_order(True, old)
+    with pytest.raises(_lib.BitrevError):
+        _lib.set_tile_order(False, 7)
+
+
 def test_version_and_counter():
     assert "sm_100a" in _lib.version()
     assert _lib.launch_count() >= 0

@@ -72,20 +72,51 @@ def test_every_tile_size(cuda, E, b):
     host = rand_bits(1 << b, E, seed=3000 * E + b)
     expected = orc.oracle_permute(host, b)
     qs = {4: [5, 6, 7], 8: [4, 5, 6], 16: [3, 4, 5, 6]}[E]
+    orders = [br.get_tile_order(False), br.get_tile_order(True)]
+    paths = [br.get_tile_path(E, False), br.get_tile_path(E, True)]
     try:
         for q in qs:
-            for inplace in (False, True):
-                br.set_tile_bits(E, inplace, q)
-            src = torch.from_numpy(host).to(cuda)
-            dst = torch.empty_like(src)
-            br.cobra_out_of_place(src, dst, br.CobraConfig(0), b)
-            br.cobra_in_place(src, br.CobraConfig(0), b)
-            torch.cuda.synchronize()
-            assert_same(dst, expected)
-            assert_same(src, expected)
+            for order in (0, 1):
+                for path in (0, 1, 2):
+                    for inplace in (False, True):
+                        br.set_tile_bits(E, inplace, q)
+                        br.set_tile_order(inplace, order)
+                        br.set_tile_path(E, inplace, path)
+                    src = torch.from_numpy(host).to(cuda)
+                    dst = torch.empty_like(src)
+                    br.cobra_out_of_place(src, dst, br.CobraConfig(0), b)
+                    br.cobra_in_place(src, br.CobraConfig(0), b)
+                    torch.cuda.synchronize()
+                    assert_same(dst, expected)
+                    assert_same(src, expected)
     finally:
         for inplace in (False, True):
             br.set_tile_bits(E, inplace, 0)
+            br.set_tile_order(inplace, orders[int(inplace)])
+            br.set_tile_path(E, inplace, paths[int(inplace)])
+
+
+@pytest.mark.parametrize("path", [0, 1, 2])
+@pytest.mark.parametrize("E", [4, 8, 16])
+@pytest.mark.parametrize("b,batch", [(14, 3), (15, 5), (19, 2), (22, 1)])
+def test_both_staging_paths(cuda, path, E, b, batch):
+    """Register-staged and TMA-bulk-staged tile kernels, batched rows, odd and
+    even widths, both families."""
+    host = rand_bits(1 << b, E, seed=6000 * E + b, batch=batch)
+    expected = orc.oracle_permute(host, b)
+    old = (br.get_tile_path(E, False), br.get_tile_path(E, True))
+    try:
+        br.set_tile_path(E, False, path)
+        br.set_tile_path(E, True, path)
+        src = torch.from_numpy(host).to(cuda)
+        out = br.bitrev_batched(src, b)
+        br.bitrev_batched_inplace(src, b)
+        torch.cuda.synchronize()
+        assert_same(out, expected)
+        assert_same(src, expected)
+    finally:
+        br.set_tile_path(E, False, old[0])
+        br.set_tile_path(E, True, old[1])
 
 
 @pytest.mark.parametrize("E", [4, 8, 16])

@@ -47,6 +47,9 @@ def main():
     ap.add_argument("--widths", type=int, nargs="+", default=[4, 8, 16])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--inplace", type=int, nargs="+", default=[0, 1])
+    ap.add_argument("--orders", type=int, nargs="+", default=[0, 1])
+    ap.add_argument("--qs", type=int, nargs="*", default=None)
+    ap.add_argument("--paths", type=int, nargs="+", default=[0, 1])
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -66,21 +69,27 @@ def main():
             dst = torch.empty_like(src)
             fl = flush if 2 * n * E < (256 << 20) else None
             for ip in args.inplace:
-                for q in QS[E]:
-                    if 2 * q > b:
+                for q in (args.qs or QS[E]):
+                    if 2 * q > b or q not in QS[E]:
                         continue
-                    br.set_tile_bits(E, bool(ip), q)
-                    if ip:
-                        fn = lambda: _core.launch_inplace(src, b)  # noqa: E731
-                    else:
-                        fn = lambda: _core.launch_oop(src, dst, b)  # noqa: E731
-                    med, best = time_it(fn, args.reps, fl)
-                    gb = 2 * n * E / 1e9
-                    print(json.dumps({"kind": "inplace" if ip else "oop", "b": b, "E": E, "q": q,
-                                      "ms_med": med * 1e3, "gbs_med": gb / med,
-                                      "gbs_best": gb / best, "l2_flushed": fl is not None}),
-                          flush=True)
+                    for order, path in [(o, p) for o in args.orders for p in args.paths]:
+                        br.set_tile_bits(E, bool(ip), q)
+                        br.set_tile_order(bool(ip), order)
+                        br.set_tile_path(E, bool(ip), path)
+                        if ip:
+                            fn = lambda: _core.launch_inplace(src, b)  # noqa: E731
+                        else:
+                            fn = lambda: _core.launch_oop(src, dst, b)  # noqa: E731
+                        med, best = time_it(fn, args.reps, fl)
+                        gb = 2 * n * E / 1e9
+                        print(json.dumps({"kind": "inplace" if ip else "oop", "b": b, "E": E,
+                                          "q": q, "order": order, "path": path,
+                                          "ms_med": med * 1e3,
+                                          "gbs_med": gb / med, "gbs_best": gb / best,
+                                          "l2_flushed": fl is not None}), flush=True)
                 br.set_tile_bits(E, bool(ip), 0)
+                br.set_tile_order(bool(ip), 0)
+                br.set_tile_path(E, bool(ip), 0)
             del src, dst
 
 
