@@ -27,14 +27,15 @@ std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_q_oop[17];
 std::atomic<int> g_q_ip[17];
 
+// Defaults from tools/tune_all.py on B200 (interleaved rounds, b = 26 and 30;
+// profiles/tune_r01.jsonl): tile bits Q and staging path per (E, family).
 int default_q(int E, bool inplace) {
   switch (E) {
-    case 4: return 6;
-    case 8: return 5;
-    case 16: return 5;
+    case 4: return inplace ? 6 : 7;
+    case 8: return inplace ? 5 : 6;
+    case 16: return inplace ? 5 : 6;
     default: return 0;
   }
-  (void)inplace;
 }
 
 bool q_supported(int E, int q) {
@@ -68,9 +69,12 @@ std::atomic<int> g_path_oop[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -
 std::atomic<int> g_path_ip[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 
 int default_path(int E, bool inplace) {
-  (void)E;
-  (void)inplace;
-  return 0;
+  switch (E) {
+    case 4: return inplace ? 2 : 0;   // TMA tensor ring / register
+    case 8: return inplace ? 2 : 1;   // TMA tensor ring / per-row bulk ring
+    case 16: return inplace ? 1 : 0;  // per-row bulk ring / register
+    default: return 0;
+  }
 }
 
 int tile_path(int E, bool inplace) {
@@ -187,48 +191,8 @@ int launch_ip_tile(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st)
   return finish_launch();
 }
 
-template <int E, int Q, bool INPLACE>
-int launch_bulk(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
-                cudaStream_t st) {
-  using B = Bulk<E, Q, INPLACE>;
-  static_assert(B::SMEM <= 227 * 1024, "bulk ring exceeds shared memory");
-  auto kern = bitrev_bulk_kernel<E, Q, INPLACE>;
-  static int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, B::SMEM);
-    return occupancy(kern, B::THREADS, B::SMEM);
-  }();
-  TileArgs a;
-  a.src = static_cast<const char*>(src);
-  a.dst = static_cast<char*>(dst);
-  a.b = b;
-  a.m = b - 2 * Q;
-  a.ntiles = (uint64_t)batch << a.m;
-  a.src_bstride = sbs * E;
-  a.dst_bstride = dbs * E;
-  a.order = tile_order(INPLACE);
-  const int grid = grid_for(a.ntiles, per_sm);
-  kern<<<grid, B::THREADS, B::SMEM, st>>>(a);
-  return finish_launch();
-}
-
-int dispatch_bulk(int E, int q, bool inplace, const void* src, void* dst, int b, int64_t batch,
-                  int64_t sbs, int64_t dbs, cudaStream_t st) {
-#define BULK(E_, Q_)                                                                   \
-  if (E == E_ && q == Q_) {                                                            \
-    return inplace ? launch_bulk<E_, Q_, true>(src, dst, b, batch, sbs, dbs, st)       \
-                   : launch_bulk<E_, Q_, false>(src, dst, b, batch, sbs, dbs, st);     \
-  }
-  BULK(4, 6) BULK(8, 5) BULK(8, 6) BULK(16, 4) BULK(16, 5)
-#undef BULK
-  if (!inplace) {
-    if (E == 4 && q == 7) return launch_bulk<4, 7, false>(src, dst, b, batch, sbs, dbs, st);
-    if (E == 16 && q == 6) return launch_bulk<16, 6, false>(src, dst, b, batch, sbs, dbs, st);
-  }
-  return BITREV_ETILE;
-}
-
 // ---------------------------------------------------------------------------
-// TMA tensor path
+// TMA ring paths (1 = per-row bulk copies, 2 = tensor-map tiles)
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -243,8 +207,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 5-D view described in bitrev_kernels.cuh (Tma family).  Returns false if
-// the driver rejects it (the caller then takes the register path).
+// 5-D view of the kTensor mode (bitrev_kernels.cuh).  Returns false if the
+// driver rejects it; the caller then takes the register path.
 bool encode_tile_map(CUtensorMap* map, const void* base, int b, int E, int q, int64_t batch,
                      int64_t bstride_elems) {
   auto fn = encode_fn();
@@ -252,7 +216,7 @@ bool encode_tile_map(CUtensorMap* map, const void* base, int b, int E, int q, in
   const int unit = E == 4 ? 4 : 8;
   const uint64_t row = (uint64_t)E << q;
   const int m = b - 2 * q;
-  if (m > 31 || batch > (int64_t(1) << 31)) return false;
+  if (m > 31 || batch > (int64_t(1) << 31) || row % 128 != 0) return false;
   cuuint64_t dims[5] = {128u / unit, (cuuint64_t)1 << q, row / 128, (cuuint64_t)1 << m,
                         (cuuint64_t)batch};
   cuuint64_t strides[4] = {(cuuint64_t)E << (b - q), 128, row,
@@ -266,17 +230,18 @@ bool encode_tile_map(CUtensorMap* map, const void* base, int b, int E, int q, in
   return r == CUDA_SUCCESS;
 }
 
-template <int E, int Q, bool INPLACE>
-int launch_tma(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
-               cudaStream_t st) {
-  using B = Tma<E, Q, INPLACE>;
-  static_assert(B::SMEM <= 227 * 1024, "tma ring exceeds shared memory");
+template <int E, int Q, bool INPLACE, int MODE>
+int launch_ring(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+                cudaStream_t st) {
+  using R = Ring<E, Q, INPLACE, MODE>;
+  static_assert(R::SMEM <= 227 * 1024, "ring exceeds shared memory");
   CUtensorMap map;
-  if (!encode_tile_map(&map, src, b, E, Q, batch, sbs)) return BITREV_ETILE;
-  auto kern = bitrev_tma_kernel<E, Q, INPLACE>;
+  memset(&map, 0, sizeof map);
+  if (MODE == kTensor && !encode_tile_map(&map, src, b, E, Q, batch, sbs)) return BITREV_ETILE;
+  auto kern = bitrev_ring_kernel<E, Q, INPLACE, MODE>;
   static int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, B::SMEM);
-    return occupancy(kern, B::THREADS, B::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, R::SMEM);
+    return occupancy(kern, R::THREADS, R::SMEM);
   }();
   TileArgs a;
   a.src = static_cast<const char*>(src);
@@ -288,30 +253,27 @@ int launch_tma(const void* src, void* dst, int b, int64_t batch, int64_t sbs, in
   a.dst_bstride = dbs * E;
   a.order = tile_order(INPLACE);
   const int grid = grid_for(a.ntiles, per_sm);
-  kern<<<grid, B::THREADS, B::SMEM, st>>>(map, a);
+  kern<<<grid, R::THREADS, R::SMEM, st>>>(map, a);
   return finish_launch();
 }
 
-int dispatch_tma(int E, int q, bool inplace, const void* src, void* dst, int b, int64_t batch,
-                 int64_t sbs, int64_t dbs, cudaStream_t st) {
-#define TMA(E_, Q_)                                                                \
-  if (E == E_ && q == Q_) {                                                        \
-    return inplace ? launch_tma<E_, Q_, true>(src, dst, b, batch, sbs, dbs, st)    \
-                   : launch_tma<E_, Q_, false>(src, dst, b, batch, sbs, dbs, st);  \
-  }
-  TMA(4, 5) TMA(4, 6) TMA(8, 4) TMA(8, 5) TMA(8, 6) TMA(16, 3) TMA(16, 4) TMA(16, 5)
-#undef TMA
-  if (!inplace) {
-    if (E == 4 && q == 7) return launch_tma<4, 7, false>(src, dst, b, batch, sbs, dbs, st);
-    if (E == 16 && q == 6) return launch_tma<16, 6, false>(src, dst, b, batch, sbs, dbs, st);
-  }
+// Instantiated (E, Q) per ring mode and family; anything else -> BITREV_ETILE.
+int dispatch_ring(int mode, int E, int q, bool inplace, const void* src, void* dst, int b,
+                  int64_t batch, int64_t sbs, int64_t dbs, cudaStream_t st) {
+#define RING(M_, E_, Q_, IP_)                                                      \
+  if (mode == M_ && E == E_ && q == Q_ && inplace == IP_)                          \
+    return launch_ring<E_, Q_, IP_, M_>(src, dst, b, batch, sbs, dbs, st);
+#define RING_BOTH(M_, E_, Q_) RING(M_, E_, Q_, false) RING(M_, E_, Q_, true)
+  RING_BOTH(kTensor, 4, 5) RING_BOTH(kTensor, 4, 6) RING_BOTH(kTensor, 8, 4)
+  RING_BOTH(kTensor, 8, 5) RING_BOTH(kTensor, 8, 6) RING_BOTH(kTensor, 16, 3)
+  RING_BOTH(kTensor, 16, 4) RING_BOTH(kTensor, 16, 5)
+  RING(kTensor, 4, 7, false) RING(kTensor, 16, 6, false)
+  RING_BOTH(kBulkRows, 4, 6) RING_BOTH(kBulkRows, 8, 5) RING_BOTH(kBulkRows, 8, 6)
+  RING_BOTH(kBulkRows, 16, 4) RING_BOTH(kBulkRows, 16, 5)
+  RING(kBulkRows, 4, 7, false) RING(kBulkRows, 16, 6, false)
+#undef RING_BOTH
+#undef RING
   return BITREV_ETILE;
-}
-
-bool bulk_supported(int E, int q, bool inplace) {
-  if ((E == 4 && q == 6) || (E == 8 && (q == 5 || q == 6)) || (E == 16 && (q == 4 || q == 5)))
-    return true;
-  return !inplace && ((E == 4 && q == 7) || (E == 16 && q == 6));
 }
 
 int dispatch_oop_tile(int E, int q, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
@@ -505,13 +467,12 @@ int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
   if (q && vec_ok) {
-    if (tile_path(E, false) == 2) {
-      const int rc2 = dispatch_tma(E, q, false, src, dst, b, batch, src_batch_stride,
-                                   dst_batch_stride, st);
+    const int path = tile_path(E, false);
+    if (path != 0) {
+      const int rc2 = dispatch_ring(path, E, q, false, src, dst, b, batch, src_batch_stride,
+                                    dst_batch_stride, st);
       if (rc2 != BITREV_ETILE) return rc2;
     }
-    if (tile_path(E, false) == 1 && bulk_supported(E, q, false))
-      return dispatch_bulk(E, q, false, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
     return dispatch_oop_tile(E, q, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
   }
   return dispatch_gather(E, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
@@ -531,12 +492,12 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
   const int q = pick_q(E, b, true);
   const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
   if (q && vec_ok) {
-    if (tile_path(E, true) == 2) {
-      const int rc2 = dispatch_tma(E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
+    const int path = tile_path(E, true);
+    if (path != 0) {
+      const int rc2 = dispatch_ring(path, E, q, true, a, a, b, batch, batch_stride, batch_stride,
+                                    st);
       if (rc2 != BITREV_ETILE) return rc2;
     }
-    if (tile_path(E, true) == 1 && bulk_supported(E, q, true))
-      return dispatch_bulk(E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
     return dispatch_ip_tile(E, q, a, b, batch, batch_stride, st);
   }
   return dispatch_swap(E, a, b, batch, batch_stride, st);

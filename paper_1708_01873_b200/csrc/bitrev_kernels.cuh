@@ -37,6 +37,12 @@
 #ifndef BITREV_MINB_OOP
 #define BITREV_MINB_OOP 1  // __launch_bounds__ min CTAs/SM, out-of-place tile kernel
 #endif
+#ifndef BITREV_EXPERIMENT_CONTIG
+#define BITREV_EXPERIMENT_CONTIG 0  // timing experiment only: partner = y ^ 1 (WRONG output)
+#endif
+#ifndef BITREV_RING_BUDGET_KB
+#define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
+#endif
 #ifndef BITREV_MINB_IP
 #define BITREV_MINB_IP 1  // __launch_bounds__ min CTAs/SM, in-place tile kernel
 #endif
@@ -305,17 +311,20 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
   uint4 r0[T::IPT][T::V], r1[T::IPT][T::V];
 
   // next work item at or after tt with y <= rev(y)
+  auto partner = [&](uint64_t y) {
+    return BITREV_EXPERIMENT_CONTIG ? (y ^ 1ull) : dev_rev(y, a.m);
+  };
   auto advance = [&](uint64_t tt) {
     while (tt < a.ntiles) {
       const uint64_t y = work_to_y(tt & mmask, a.m, a.order);
-      if (dev_rev(y, a.m) >= y) break;
+      if (partner(y) >= y) break;
       tt += gridDim.x;
     }
     return tt;
   };
   auto issue = [&](uint64_t tt) {
     const uint64_t bi = tt >> a.m, y = work_to_y(tt & mmask, a.m, a.order),
-                   ry = dev_rev(y, a.m);
+                   ry = partner(y);
     const char* base = a.src + bi * a.src_bstride;
     tile_load<E, Q, BITREV_IP_NC>(r0, base + (y << Q) * E, row_stride);
     if (ry != y) tile_load<E, Q, BITREV_IP_NC>(r1, base + (ry << Q) * E, row_stride);
@@ -325,8 +334,7 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
   if (t >= a.ntiles) return;
   issue(t);
   for (;;) {
-    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order),
-                   ry = dev_rev(y, a.m);
+    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order), ry = partner(y);
     const bool pair = ry != y;
     tile_stage<E, Q>(r0, U0);
     if (pair) tile_stage<E, Q>(r1, U1);
@@ -343,274 +351,164 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
 }
 
 // ---------------------------------------------------------------------------
-// TMA bulk-copy family: cp.async.bulk row copies into a multi-stage smem ring
+// TMA ring family: warp-specialised producer / consumers over an smem ring
 //
-// The register-staged kernels above hold every in-flight byte in registers,
-// which caps the bytes in flight per SM (occupancy is register-limited) and
-// leaves the in-place kernel latency-bound.  Here each tile row (2^Q*E
-// contiguous bytes) is one `cp.async.bulk.shared::cluster.global` copy that
-// completes on a per-stage mbarrier; a CTA keeps NS-1 work items loading
-// while it drains the oldest, so in-flight bytes cost shared memory only.
+// The register-staged kernels hold every in-flight byte in registers, so
+// bytes in flight per SM are register-limited and each CTA alternates
+// load -> barrier -> drain.  Here one producer warp streams tiles into an
+// NS-stage shared-memory ring with TMA, and NCW consumer warps drain them;
+// stages are handed over with mbarriers (full: TMA transaction bytes; empty:
+// one arrival per consumer warp), so no block-wide barrier sits in the loop.
 //
-// Shared layout per tile: row x at x*PITCH, PITCH = 2^Q*E + 16 (the 16-byte
-// pad rotates consecutive rows across the 8 bank groups).  The drain is the
-// register-staged kernel's transpose moved to the read side: a thread reads
-// the 16-byte chunk c of the V rows g + k*2^Q/V (consecutive lanes take
-// consecutive g: conflict-free LDS.128), transposes V x V in registers, and
-// writes V vectors to destination rows rev_Q(c*V + j) at chunk rev(g) (a warp
-// covers whole contiguous destination rows).
+// Two ways to fill a stage (template MODE):
+//   kBulkRows  one cp.async.bulk per tile row (2^Q*E bytes) into padded rows
+//              (PITCH = row + 16 B rotates rows across bank groups);
+//   kTensor    ONE cp.async.bulk.tensor per tile through a 5-D tensor map
+//                d0: 128-byte unit run   (unit = 4 B for E = 4, else 8 B)
+//                d1: tile row x          stride 2^(b-Q) * E
+//                d2: 128-byte piece      stride 128 B
+//                d3: middle value y      stride 2^Q * E
+//                d4: batch row           stride batch_stride * E
+//              box {128/unit, 2^Q, pieces, 1, 1} = tile y; SWIZZLE_128B puts
+//              16-byte chunk cc of segment R = piece * 2^Q + x at cc ^ (x & 7).
+// The drain is the register kernel's transpose moved to the read side: a lane
+// reads chunk c of the V rows g + k*2^Q/V (consecutive lanes = consecutive g:
+// conflict-free LDS.128), transposes V x V in registers and writes V vectors
+// to destination rows rev_Q(c*V + j) at chunk rev(g) (a warp writes whole
+// contiguous destination rows).
+
+constexpr int kBulkRows = 1;
+constexpr int kTensor = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_fence_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
+      "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, int c3, int c4,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %2, %2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(tmap), "r"(0), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
 
-template <int E, int Q, bool INPLACE>
-struct Bulk {
+template <int E, int Q, bool INPLACE, int MODE>
+struct Ring {
   static constexpr int S = 1 << Q;
   static constexpr int V = 16 / E;
   static constexpr int LV = const_log2(V);
-  static constexpr int G = S / V;              // row groups == 16-byte chunks per row
-  static constexpr int ROW = S * E;            // bytes per tile row
-  static constexpr int PITCH = ROW + 16;
-  static constexpr int TILE = S * PITCH;       // smem bytes per staged tile
+  static constexpr int G = S / V;               // row groups == 16-byte chunks per row
+  static constexpr int ROW = S * E;             // bytes per tile row
+  static constexpr int PITCH = MODE == kTensor ? ROW : ROW + 16;
+  static constexpr int TILE = S * PITCH;
   static constexpr int TILES = INPLACE ? 2 : 1;
   static constexpr int STAGE = TILES * TILE;
-  static constexpr int NS_RAW = 98304 / STAGE;
-  static constexpr int NS = NS_RAW < 2 ? 2 : (NS_RAW > 8 ? 8 : NS_RAW);  // ring depth
-  static constexpr int ITEMS = G * G;          // drain items (V chunks each)
-  static constexpr int THREADS = ITEMS < 256 ? ITEMS : 256;
-  static constexpr int IPT = ITEMS / THREADS;
-  static constexpr int SMEM = NS * STAGE + NS * 8;
-  static_assert(E == 4 || E == 8 || E == 16, "bulk kernels move 4/8/16-byte elements");
+  static constexpr int BUDGET = BITREV_RING_BUDGET_KB * 1024;  // ring bytes per CTA
+  static constexpr int NS_RAW = BUDGET / STAGE;
+  static constexpr int NS = NS_RAW < 2 ? 2 : (NS_RAW > 16 ? 16 : NS_RAW);
+  static constexpr int ITEMS = G * G;           // drain items per tile (V chunks each)
+  static constexpr int NCW_RAW = ITEMS / 32;
+  static constexpr int NCW = NCW_RAW > 8 ? 8 : NCW_RAW;  // consumer warps
+  static constexpr int THREADS = 32 * (NCW + 1);
+  static constexpr int IPW = ITEMS / (32 * NCW);          // drain items per lane per tile
+  static constexpr int SMEM = NS * STAGE + 1024 + 2 * NS * 8;
+  static_assert(E == 4 || E == 8 || E == 16, "ring kernels move 4/8/16-byte elements");
   static_assert(G >= 8 && ROW % 16 == 0, "chunk geometry");
-  static_assert(ITEMS % THREADS == 0 && THREADS >= 32, "even split");
-  static_assert(S <= 32 * 4, "rows per tile issued by one warp");
+  static_assert(MODE != kTensor || ROW % 128 == 0, "tensor tiles need 128-byte rows");
+  static_assert(NCW >= 1 && ITEMS % (32 * NCW) == 0, "even split");
 };
 
-template <int E, int Q, bool INPLACE>
-__device__ __forceinline__ void bulk_drain(const unsigned char* tile, char* dst_base,
-                                           uint64_t row_stride) {
-  using B = Bulk<E, Q, INPLACE>;
+template <int E, int Q, bool INPLACE, int MODE>
+__device__ __forceinline__ void ring_drain(uint32_t tile, char* dst_base, uint64_t row_stride,
+                                           int cw, int lane) {
+  using R = Ring<E, Q, INPLACE, MODE>;
 #pragma unroll
-  for (int it = 0; it < B::IPT; ++it) {
-    const int id = it * B::THREADS + threadIdx.x;
-    const int g = id % B::G;
-    const int c = id / B::G;
-    uint4 v[B::V];
+  for (int it = 0; it < R::IPW; ++it) {
+    const int id = (it * R::NCW + cw) * 32 + lane;
+    const int g = id % R::G;
+    const int c = id / R::G;
+    uint4 v[R::V];
 #pragma unroll
-    for (int k = 0; k < B::V; ++k)
-      v[k] = *reinterpret_cast<const uint4*>(tile + (g + k * B::G) * B::PITCH + c * 16);
-    const uint64_t col = __brev((unsigned)g) >> (32 - (Q - B::LV));
-    char* base = dst_base + col * 16;
-    if constexpr (B::V == 1) {
-      st_vec(base + (uint64_t)(__brev((unsigned)c) >> (32 - Q)) * row_stride, xpose<E, 0>(v));
-    } else if constexpr (B::V == 2) {
-      st_vec(base + (uint64_t)(__brev((unsigned)(c * 2 + 0)) >> (32 - Q)) * row_stride,
-             xpose<E, 0>(v));
-      st_vec(base + (uint64_t)(__brev((unsigned)(c * 2 + 1)) >> (32 - Q)) * row_stride,
+    for (int k = 0; k < R::V; ++k) {
+      const int x = g + k * R::G;
+      uint32_t addr;
+      if constexpr (MODE == kTensor)
+        addr = tile + ((c >> 3) * R::S + x) * 128 + (((c & 7) ^ (x & 7)) << 4);
+      else
+        addr = tile + x * R::PITCH + c * 16;
+      v[k] = lds128(addr);
+    }
+    char* base = dst_base + (uint64_t)(__brev((unsigned)g) >> (32 - (Q - R::LV))) * 16;
+    st_vec(base + (uint64_t)(__brev((unsigned)(c * R::V)) >> (32 - Q)) * row_stride,
+           xpose<E, 0>(v));
+    if constexpr (R::V > 1)
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * R::V + 1)) >> (32 - Q)) * row_stride,
              xpose<E, 1>(v));
-    } else {
-      st_vec(base + (uint64_t)(__brev((unsigned)(c * 4 + 0)) >> (32 - Q)) * row_stride,
-             xpose<E, 0>(v));
-      st_vec(base + (uint64_t)(__brev((unsigned)(c * 4 + 1)) >> (32 - Q)) * row_stride,
-             xpose<E, 1>(v));
-      st_vec(base + (uint64_t)(__brev((unsigned)(c * 4 + 2)) >> (32 - Q)) * row_stride,
+    if constexpr (R::V > 2) {
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * R::V + 2)) >> (32 - Q)) * row_stride,
              xpose<E, 2>(v));
-      st_vec(base + (uint64_t)(__brev((unsigned)(c * 4 + 3)) >> (32 - Q)) * row_stride,
+      st_vec(base + (uint64_t)(__brev((unsigned)(c * R::V + 3)) >> (32 - Q)) * row_stride,
              xpose<E, 3>(v));
     }
   }
 }
 
-// Persistent ring kernel.  Out of place: one item = one tile y.  In place: one
-// item = the tile pair {y, rev(y)} with y <= rev(y) (both tiles staged before
-// either is written, as in the register kernel).  Warp 0 is also the producer:
-// at iteration i it refills the slot drained at iteration i-1 (released by the
-// barrier that ends every iteration) with item i+NS-1.
-template <int E, int Q, bool INPLACE>
-__global__ void __launch_bounds__(Bulk<E, Q, INPLACE>::THREADS)
-    bitrev_bulk_kernel(TileArgs a) {
-  using B = Bulk<E, Q, INPLACE>;
-  extern __shared__ __align__(128) unsigned char smem_b[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_b + B::NS * B::STAGE);
+// Persistent ring kernel.  Out of place: one work item = tile y.  In place:
+// one item = the pair {y, rev(y)} with y <= rev(y); both tiles are staged
+// before either is drained, and the pair's regions are touched by no other
+// item, so the in-place hazard is confined to the item.
+template <int E, int Q, bool INPLACE, int MODE>
+__global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
+    bitrev_ring_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a) {
+  using R = Ring<E, Q, INPLACE, MODE>;
+  extern __shared__ __align__(1024) unsigned char smem_ring[];
+  const uint32_t base =
+      (smem_u32(smem_ring) + 1023u) & ~1023u;  // 1024-B alignment for the 128B swizzle
+  const uint32_t full = base + R::NS * R::STAGE;
+  const uint32_t empty = full + R::NS * 8;
   const uint64_t row_stride = (uint64_t)E << (a.b - Q);
   const uint64_t mmask = (1ull << a.m) - 1;
-
-  auto valid_item = [&](uint64_t tt) {
-    if constexpr (!INPLACE) return true;
-    const uint64_t y = work_to_y(tt & mmask, a.m, a.order);
-    return dev_rev(y, a.m) >= y;
-  };
-  auto advance = [&](uint64_t tt) {
-    while (tt < a.ntiles && !valid_item(tt)) tt += gridDim.x;
-    return tt;
-  };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < B::NS; ++s) mbar_init(&bars[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  const bool producer = threadIdx.x < 32;
-  const int lane = threadIdx.x & 31;
-  uint64_t tp = advance(blockIdx.x);  // producer's next item (warp 0 only)
-  auto produce = [&](int slot) {
-    if (tp >= a.ntiles) return;
-    const uint64_t bi = tp >> a.m, y = work_to_y(tp & mmask, a.m, a.order);
-    const uint64_t ry = dev_rev(y, a.m);
-    const bool pair = INPLACE && ry != y;
-    unsigned char* st = smem_b + slot * B::STAGE;
-    const char* base = a.src + bi * a.src_bstride;
-    if (lane == 0) mbar_expect_tx(&bars[slot], (pair ? 2 : 1) * B::S * B::ROW);
-    __syncwarp();
-    for (int x = lane; x < B::S; x += 32) {
-      bulk_g2s(st + x * B::PITCH, base + x * row_stride + (y << Q) * E, B::ROW, &bars[slot]);
-      if (pair)
-        bulk_g2s(st + B::TILE + x * B::PITCH, base + x * row_stride + (ry << Q) * E, B::ROW,
-                 &bars[slot]);
-    }
-    tp = advance(tp + gridDim.x);
-  };
-  if (producer)
-    for (int s = 0; s < B::NS - 1; ++s) produce(s);
-
-  uint64_t t = advance(blockIdx.x);
-  for (int i = 0; t < a.ntiles; ++i) {
-    const int slot = i % B::NS;
-    if (producer) produce((i + B::NS - 1) % B::NS);
-    mbar_wait(&bars[slot], (uint32_t)((i / B::NS) & 1));
-    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
-    const uint64_t ry = dev_rev(y, a.m);
-    const unsigned char* st = smem_b + slot * B::STAGE;
-    char* dbase = a.dst + bi * a.dst_bstride;
-    bulk_drain<E, Q, INPLACE>(st, dbase + (ry << Q) * E, row_stride);
-    if (INPLACE && ry != y) bulk_drain<E, Q, INPLACE>(st + B::TILE, dbase + (y << Q) * E, row_stride);
-    __syncthreads();
-    t = advance(t + gridDim.x);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// TMA tensor family: one cp.async.bulk.tensor per tile
-//
-// The 1-D bulk family needs one copy instruction per tile row, and
-// cp.async.bulk takes uniform operands, so 32 lanes issuing their own rows
-// serialise through an ELECT loop (ncu: the producer warp dominates every
-// iteration).  Here the array is described by a 5-D tensor map
-//     d0: 128-byte unit run   (unit = 4 B for E = 4, else 8 B)
-//     d1: tile row x          stride 2^(b-Q) * E
-//     d2: 128-byte piece      stride 128 B          (2^Q*E / 128 pieces)
-//     d3: middle value y      stride 2^Q * E
-//     d4: batch row           stride batch_stride * E
-// so the box {128/unit, 2^Q, pieces, 1, 1} at (0, 0, 0, y, batch) is exactly
-// tile y, fetched by ONE instruction.  With CU_TENSOR_MAP_SWIZZLE_128B the
-// 16-byte chunk cc of 128-byte segment R = piece * 2^Q + x lands at chunk
-// cc ^ (x & 7): lanes reading consecutive rows x hit 8 distinct bank groups.
-
-template <int E, int Q, bool INPLACE>
-struct Tma {
-  static constexpr int S = 1 << Q;
-  static constexpr int V = 16 / E;
-  static constexpr int LV = const_log2(V);
-  static constexpr int G = S / V;
-  static constexpr int ROW = S * E;
-  static constexpr int P = ROW / 128;          // 128-byte pieces per row
-  static constexpr int TILE = S * ROW;         // dense, 1024-byte aligned
-  static constexpr int TILES = INPLACE ? 2 : 1;
-  static constexpr int STAGE = TILES * TILE;
-  static constexpr int NS_RAW = 98304 / STAGE;
-  static constexpr int NS = NS_RAW < 2 ? 2 : (NS_RAW > 8 ? 8 : NS_RAW);
-  static constexpr int ITEMS = G * G;
-  static constexpr int THREADS = ITEMS < 256 ? ITEMS : 256;
-  static constexpr int IPT = ITEMS / THREADS;
-  static constexpr int SMEM = NS * STAGE + 1024 + NS * 8;  // + alignment slack
-  static_assert(ROW % 128 == 0 && S >= 8, "tensor tiles need 128-byte rows");
-  static_assert(ITEMS % THREADS == 0 && THREADS >= 32, "even split");
-};
-
-__device__ __forceinline__ void tma_load_5d(void* dst, const void* tmap, int c0, int c1, int c2,
-                                            int c3, int c4, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
-      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <int E, int Q, bool INPLACE>
-__device__ __forceinline__ void tma_drain(const unsigned char* tile, char* dst_base,
-                                          uint64_t row_stride) {
-  using B = Tma<E, Q, INPLACE>;
-#pragma unroll
-  for (int it = 0; it < B::IPT; ++it) {
-    const int id = it * B::THREADS + threadIdx.x;
-    const int g = id % B::G;
-    const int c = id / B::G;
-    const int piece = c >> 3, cc = c & 7;
-    uint4 v[B::V];
-#pragma unroll
-    for (int k = 0; k < B::V; ++k) {
-      const int x = g + k * B::G;
-      v[k] = *reinterpret_cast<const uint4*>(tile + (piece * B::S + x) * 128 +
-                                             ((cc ^ (x & 7)) << 4));
-    }
-    const uint64_t col = __brev((unsigned)g) >> (32 - (Q - B::LV));
-    char* base = dst_base + col * 16;
-#pragma unroll
-    for (int j = 0; j < B::V; ++j) {
-      uint4 w;
-      if (j == 0) w = xpose<E, 0>(v);
-      if constexpr (B::V > 1) { if (j == 1) w = xpose<E, 1>(v); }
-      if constexpr (B::V > 2) {
-        if (j == 2) w = xpose<E, 2>(v);
-        if (j == 3) w = xpose<E, 3>(v);
-      }
-      st_vec(base + (uint64_t)(__brev((unsigned)(c * B::V + j)) >> (32 - Q)) * row_stride, w);
-    }
-  }
-}
-
-template <int E, int Q, bool INPLACE>
-__global__ void __launch_bounds__(Tma<E, Q, INPLACE>::THREADS)
-    bitrev_tma_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a) {
-  using B = Tma<E, Q, INPLACE>;
-  extern __shared__ __align__(1024) unsigned char smem_t_raw[];
-  unsigned char* smem_t = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_t_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_t + B::NS * B::STAGE);
-  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
-  const uint64_t mmask = (1ull << a.m) - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   auto advance = [&](uint64_t tt) {
     if constexpr (INPLACE) {
@@ -624,40 +522,62 @@ __global__ void __launch_bounds__(Tma<E, Q, INPLACE>::THREADS)
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < B::NS; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < R::NS; ++s) {
+      mbar_init(full + 8 * s, 1);
+      mbar_init(empty + 8 * s, R::NCW);
+    }
     mbar_fence_init();
   }
   __syncthreads();
 
-  uint64_t tp = advance(blockIdx.x);  // producer (thread 0) cursor
-  auto produce = [&](int slot) {
-    if (tp >= a.ntiles) return;
-    const uint64_t y = work_to_y(tp & mmask, a.m, a.order);
-    const int bi = (int)(tp >> a.m);
-    const uint64_t ry = dev_rev(y, a.m);
-    const bool pair = INPLACE && ry != y;
-    unsigned char* st = smem_t + slot * B::STAGE;
-    mbar_expect_tx(&bars[slot], (pair ? 2 : 1) * B::TILE);
-    tma_load_5d(st, &tmap, 0, 0, 0, (int)y, bi, &bars[slot]);
-    if (pair) tma_load_5d(st + B::TILE, &tmap, 0, 0, 0, (int)ry, bi, &bars[slot]);
-    tp = advance(tp + gridDim.x);
-  };
-  if (threadIdx.x == 0)
-    for (int s = 0; s < B::NS - 1; ++s) produce(s);
-
-  uint64_t t = advance(blockIdx.x);
-  for (int i = 0; t < a.ntiles; ++i) {
-    const int slot = i % B::NS;
-    if (threadIdx.x == 0) produce((i + B::NS - 1) % B::NS);
-    mbar_wait(&bars[slot], (uint32_t)((i / B::NS) & 1));
-    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
-    const uint64_t ry = dev_rev(y, a.m);
-    const unsigned char* st = smem_t + slot * B::STAGE;
-    char* dbase = a.dst + bi * a.dst_bstride;
-    tma_drain<E, Q, INPLACE>(st, dbase + (ry << Q) * E, row_stride);
-    if (INPLACE && ry != y) tma_drain<E, Q, INPLACE>(st + B::TILE, dbase + (y << Q) * E, row_stride);
-    __syncthreads();
-    t = advance(t + gridDim.x);
+  if (warp == R::NCW) {
+    // ---- producer warp
+    uint64_t t = advance(blockIdx.x);
+    for (int i = 0; t < a.ntiles; ++i) {
+      const int s = i % R::NS;
+      if (i >= R::NS) mbar_wait(empty + 8 * s, (uint32_t)(((i / R::NS) - 1) & 1));
+      const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
+      const uint64_t ry = dev_rev(y, a.m);
+      const bool pair = INPLACE && ry != y;
+      const uint32_t st = base + s * R::STAGE;
+      const uint32_t bar = full + 8 * s;
+      if constexpr (MODE == kTensor) {
+        if (lane == 0) {
+          mbar_expect_tx(bar, (pair ? 2 : 1) * R::S * R::ROW);
+          tma_load_5d(st, &tmap, (int)y, (int)bi, bar);
+          if (pair) tma_load_5d(st + R::TILE, &tmap, (int)ry, (int)bi, bar);
+        }
+      } else {
+        if (lane == 0) mbar_expect_tx(bar, (pair ? 2 : 1) * R::S * R::ROW);
+        __syncwarp();
+        const char* src = a.src + bi * a.src_bstride;
+        for (int x = lane; x < R::S; x += 32) {
+          bulk_g2s(st + x * R::PITCH, src + x * row_stride + (y << Q) * E, R::ROW, bar);
+          if (pair)
+            bulk_g2s(st + R::TILE + x * R::PITCH, src + x * row_stride + (ry << Q) * E, R::ROW,
+                     bar);
+        }
+      }
+      t = advance(t + gridDim.x);
+    }
+  } else {
+    // ---- consumer warps
+    uint64_t t = advance(blockIdx.x);
+    for (int i = 0; t < a.ntiles; ++i) {
+      const int s = i % R::NS;
+      mbar_wait(full + 8 * s, (uint32_t)((i / R::NS) & 1));
+      const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
+      const uint64_t ry = dev_rev(y, a.m);
+      const uint32_t st = base + s * R::STAGE;
+      char* dbase = a.dst + bi * a.dst_bstride;
+      ring_drain<E, Q, INPLACE, MODE>(st, dbase + (ry << Q) * E, row_stride, warp, lane);
+      if (INPLACE && ry != y)
+        ring_drain<E, Q, INPLACE, MODE>(st + R::TILE, dbase + (y << Q) * E, row_stride, warp,
+                                        lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + 8 * s);
+      t = advance(t + gridDim.x);
+    }
   }
 }
 
