@@ -1,0 +1,42 @@
+"""The C ABI driven exactly as INTEGRATION.md's ctypes stub does it: plain
+ctypes on numpy arrays, host entry points, NULL device scratch, no torch."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1708_01873_b200._lib import LIB_PATH
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib(cuda):
+    L = ctypes.CDLL(str(LIB_PATH))
+    vp, i, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    L.bitrev_oop_host.argtypes = [vp, vp, i, i, i64, vp, vp, vp]
+    L.bitrev_inplace_host.argtypes = [vp, i, i, i64, vp, vp]
+    L.bitrev_strerror.restype = ctypes.c_char_p
+    return L
+
+
+@pytest.mark.parametrize("E,dt", [(4, np.float32), (8, np.float64), (16, np.complex128),
+                                  (2, np.int16), (1, np.uint8)])
+@pytest.mark.parametrize("b", [3, 12, 17, 21])
+def test_stub_copy_and_swap(lib, E, dt, b):
+    x = np.random.default_rng(b * 17 + E).integers(0, 256, (1 << b) * E, dtype=np.uint8).view(dt)
+    expected = orc.oracle_permute(x, b).view(np.uint8)
+    dst = np.empty_like(x)
+    assert lib.bitrev_oop_host(x.ctypes.data, dst.ctypes.data, b, E, 1, None, None, None) == 0
+    assert np.array_equal(dst.view(np.uint8), expected)
+    a = x.copy()
+    assert lib.bitrev_inplace_host(a.ctypes.data, b, E, 1, None, None) == 0
+    assert np.array_equal(a.view(np.uint8), expected)
+
+
+def test_stub_reports_errors(lib):
+    x = np.zeros(16, dtype=np.float64)
+    rc = lib.bitrev_inplace_host(x.ctypes.data, 60, 8, 1, None, None)
+    assert rc < 0 and b"width" in lib.bitrev_strerror(rc)
