@@ -28,11 +28,11 @@ std::atomic<int> g_q_oop[17];
 std::atomic<int> g_q_ip[17];
 
 // Defaults from tools/tune_all.py on B200 (interleaved rounds, b = 26 and 30;
-// profiles/tune_r01.jsonl): tile bits Q and staging path per (E, family).
+// profiles/tune_r01*.jsonl): tile bits Q and staging path per (E, family).
 int default_q(int E, bool inplace) {
   switch (E) {
     case 4: return inplace ? 6 : 7;
-    case 8: return inplace ? 5 : 6;
+    case 8: return 6;
     case 16: return inplace ? 5 : 6;
     default: return 0;
   }
@@ -40,9 +40,9 @@ int default_q(int E, bool inplace) {
 
 bool q_supported(int E, int q) {
   switch (E) {
-    case 4: return q >= 5 && q <= 7;
-    case 8: return q >= 4 && q <= 6;
-    case 16: return q >= 3 && q <= 6;
+    case 4: return q >= 5 && q <= 8;
+    case 8: return q >= 4 && q <= 7;
+    case 16: return q >= 3 && q <= 7;
     default: return false;
   }
 }
@@ -69,11 +69,10 @@ std::atomic<int> g_path_oop[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -
 std::atomic<int> g_path_ip[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 
 int default_path(int E, bool inplace) {
+  if (inplace) return 0;  // register tile pairs (compact pair enumeration)
   switch (E) {
-    case 4: return inplace ? 2 : 0;   // TMA tensor ring / register
-    case 8: return inplace ? 2 : 1;   // TMA tensor ring / per-row bulk ring
-    case 16: return inplace ? 1 : 0;  // per-row bulk ring / register
-    default: return 0;
+    case 8: return 1;     // per-row cp.async.bulk ring
+    default: return 0;    // register tiles
   }
 }
 
@@ -92,7 +91,8 @@ int tile_order(bool inplace) {
   std::atomic<int>& o = inplace ? g_order_ip : g_order_oop;
   int v = o.load();
   if (v < 0) {
-    v = env_int(inplace ? "BITREV_B200_ORDER_IP" : "BITREV_B200_ORDER_OOP", 0);
+    // in place: compact pair enumeration (2); out of place: y = work index (0)
+    v = env_int(inplace ? "BITREV_B200_ORDER_IP" : "BITREV_B200_ORDER_OOP", inplace ? 2 : 0);
     o.store(v);
   }
   return v;
@@ -133,6 +133,42 @@ int grid_for(uint64_t work, int per_sm, int threads_hint = 0) {
   return (int)(g > 0 ? g : 1);
 }
 
+// In-place work items: tile order 2 = compact pair enumeration
+// (pair_from_index: one item per unordered pair, walked with a division-free
+// cursor); other orders visit every y and skip items with rev(y) < y.
+bool compact_pairs() { return tile_order(true) == 2; }
+
+int grid_for_pairs(uint64_t work, int per_sm);
+
+// Fills the work fields of an in-place launch; returns the grid size.
+int set_pair_work(TileArgs& a, int64_t batch, bool compact, int per_sm) {
+  a.batch = batch;
+  if (!compact) {
+    a.npairs = 0;
+    a.step_b = a.step_w = 0;
+    a.ntiles = (uint64_t)batch << a.m;
+    return grid_for_pairs(a.ntiles, per_sm);
+  }
+  a.npairs = pair_count(a.m);
+  a.ntiles = (uint64_t)batch * a.npairs;
+  const int grid = grid_for(a.ntiles, per_sm);  // every item is real work: no parity trick
+  a.step_b = (uint64_t)grid / a.npairs;
+  a.step_w = (uint64_t)grid % a.npairs;
+  return grid;
+}
+
+// Persistent grid for the in-place pair kernels.  CTA j visits work items
+// j, j+G, j+2G, ...; an item is skipped when rev(y) < y, and that depends on
+// y's low bits.  With an even G every CTA sees a fixed residue of y's low
+// bits, so skip rates (and CTA run times) differ by up to ~2x -- ncu showed
+// SMs active 61 % of the elapsed cycles.  An odd G cycles every CTA through
+// all residues.
+int grid_for_pairs(uint64_t work, int per_sm) {
+  int g = grid_for(work, per_sm);
+  if (g > 1 && (g & 1) == 0) --g;
+  return g;
+}
+
 // Resident CTAs per SM of a kernel at a dynamic smem size (cached per instance
 // by the caller through a function-local static).
 template <typename K>
@@ -164,15 +200,17 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
   a.src_bstride = sbs * E;
   a.dst_bstride = dbs * E;
   a.order = tile_order(false);
+  a.npairs = 0;
+  a.batch = batch;
   const int grid = grid_for(a.ntiles, per_sm);
   kern<<<grid, T::THREADS, T::BYTES, st>>>(a);
   return finish_launch();
 }
 
-template <int E, int Q>
-int launch_ip_tile(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+template <int E, int Q, bool COMPACT>
+int launch_ip_tile_mode(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
   using T = Tile<E, Q>;
-  auto kern = bitrev_inplace_tile_kernel<E, Q>;
+  auto kern = bitrev_inplace_tile_kernel<E, Q, COMPACT>;
   static int per_sm = [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * T::BYTES);
     return occupancy(kern, T::THREADS, 2 * T::BYTES);
@@ -182,13 +220,18 @@ int launch_ip_tile(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st)
   a.dst = static_cast<char*>(buf);
   a.b = b;
   a.m = b - 2 * Q;
-  a.ntiles = (uint64_t)batch << a.m;
   a.src_bstride = bs * E;
   a.dst_bstride = bs * E;
   a.order = tile_order(true);
-  const int grid = grid_for(a.ntiles, per_sm);
+  const int grid = set_pair_work(a, batch, COMPACT, per_sm);
   kern<<<grid, T::THREADS, 2 * T::BYTES, st>>>(a);
   return finish_launch();
+}
+
+template <int E, int Q>
+int launch_ip_tile(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  return compact_pairs() ? launch_ip_tile_mode<E, Q, true>(buf, b, batch, bs, st)
+                         : launch_ip_tile_mode<E, Q, false>(buf, b, batch, bs, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -230,15 +273,15 @@ bool encode_tile_map(CUtensorMap* map, const void* base, int b, int E, int q, in
   return r == CUDA_SUCCESS;
 }
 
-template <int E, int Q, bool INPLACE, int MODE>
-int launch_ring(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
-                cudaStream_t st) {
+template <int E, int Q, bool INPLACE, int MODE, bool COMPACT>
+int launch_ring_mode(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+                     cudaStream_t st) {
   using R = Ring<E, Q, INPLACE, MODE>;
   static_assert(R::SMEM <= 227 * 1024, "ring exceeds shared memory");
   CUtensorMap map;
   memset(&map, 0, sizeof map);
   if (MODE == kTensor && !encode_tile_map(&map, src, b, E, Q, batch, sbs)) return BITREV_ETILE;
-  auto kern = bitrev_ring_kernel<E, Q, INPLACE, MODE>;
+  auto kern = bitrev_ring_kernel<E, Q, INPLACE, MODE, COMPACT>;
   static int per_sm = [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, R::SMEM);
     return occupancy(kern, R::THREADS, R::SMEM);
@@ -252,9 +295,24 @@ int launch_ring(const void* src, void* dst, int b, int64_t batch, int64_t sbs, i
   a.src_bstride = sbs * E;
   a.dst_bstride = dbs * E;
   a.order = tile_order(INPLACE);
-  const int grid = grid_for(a.ntiles, per_sm);
+  a.npairs = 0;
+  a.batch = batch;
+  int grid;
+  if (INPLACE) {
+    grid = set_pair_work(a, batch, COMPACT, per_sm);
+  } else {
+    grid = grid_for(a.ntiles, per_sm);
+  }
   kern<<<grid, R::THREADS, R::SMEM, st>>>(map, a);
   return finish_launch();
+}
+
+template <int E, int Q, bool INPLACE, int MODE>
+int launch_ring(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+                cudaStream_t st) {
+  if (INPLACE && compact_pairs())
+    return launch_ring_mode<E, Q, INPLACE, MODE, true>(src, dst, b, batch, sbs, dbs, st);
+  return launch_ring_mode<E, Q, INPLACE, MODE, false>(src, dst, b, batch, sbs, dbs, st);
 }
 
 // Instantiated (E, Q) per ring mode and family; anything else -> BITREV_ETILE.
@@ -273,6 +331,57 @@ int dispatch_ring(int mode, int E, int q, bool inplace, const void* src, void* d
   RING(kBulkRows, 4, 7, false) RING(kBulkRows, 16, 6, false)
 #undef RING_BOTH
 #undef RING
+  return BITREV_ETILE;
+}
+
+// Rectangular out-of-place tiles: path 3 (QX = long destination side).
+template <int E, int QX, int QZ>
+int launch_oop_rect(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
+                    cudaStream_t st) {
+  using T = Rect<E, QX, QZ>;
+  if (b < QX + QZ) return BITREV_ETILE;
+  auto kern = bitrev_oop_rect_kernel<E, QX, QZ>;
+  static int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES);
+    return occupancy(kern, T::THREADS, T::BYTES);
+  }();
+  TileArgs a;
+  a.src = static_cast<const char*>(src);
+  a.dst = static_cast<char*>(dst);
+  a.b = b;
+  a.m = b - QX - QZ;
+  a.ntiles = (uint64_t)batch << a.m;
+  a.src_bstride = sbs * E;
+  a.dst_bstride = dbs * E;
+  a.order = tile_order(false);
+  a.npairs = 0;
+  a.batch = batch;
+  const int grid = grid_for(a.ntiles, per_sm);
+  kern<<<grid, T::THREADS, T::BYTES, st>>>(a);
+  return finish_launch();
+}
+
+// q selects the destination run (QX); QZ is the 128-byte source piece.
+int dispatch_oop_rect(int E, int q, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
+                      int64_t dbs, cudaStream_t st) {
+  switch (E) {
+    case 4:
+      if (q == 6) return launch_oop_rect<4, 6, 5>(src, dst, b, batch, sbs, dbs, st);
+      if (q == 7) return launch_oop_rect<4, 7, 5>(src, dst, b, batch, sbs, dbs, st);
+      if (q == 8) return launch_oop_rect<4, 8, 5>(src, dst, b, batch, sbs, dbs, st);
+      break;
+    case 8:
+      if (q == 5) return launch_oop_rect<8, 5, 4>(src, dst, b, batch, sbs, dbs, st);
+      if (q == 6) return launch_oop_rect<8, 6, 4>(src, dst, b, batch, sbs, dbs, st);
+      if (q == 7) return launch_oop_rect<8, 7, 4>(src, dst, b, batch, sbs, dbs, st);
+      break;
+    case 16:
+      if (q == 4) return launch_oop_rect<16, 4, 3>(src, dst, b, batch, sbs, dbs, st);
+      if (q == 5) return launch_oop_rect<16, 5, 3>(src, dst, b, batch, sbs, dbs, st);
+      if (q == 6) return launch_oop_rect<16, 6, 3>(src, dst, b, batch, sbs, dbs, st);
+      if (q == 7) return launch_oop_rect<16, 7, 3>(src, dst, b, batch, sbs, dbs, st);
+      break;
+  }
   return BITREV_ETILE;
 }
 
@@ -417,11 +526,12 @@ int check_common(int b, int E, int64_t batch) {
   return BITREV_OK;
 }
 
-// Pick the tile bits for (E, b): the configured q, reduced so that 2q <= b.
+// Tile bits for (E, b): the configured q, reduced so that 2q <= b (the
+// dispatchers then walk further down to the largest instantiated width).
 int pick_q(int E, int b, bool inplace) {
   int q = current_q(E, inplace);
   while (q > 0 && 2 * q > b) --q;
-  return q_supported(E, q) ? q : 0;
+  return q;
 }
 
 }  // namespace
@@ -463,17 +573,26 @@ int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (n * E <= kSmallBytes) return dispatch_small(E, src, dst, b, batch, src_batch_stride,
                                                    dst_batch_stride, st);
-  const int q = pick_q(E, b, false);
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
-  if (q && vec_ok) {
+  if (vec_ok && (E == 4 || E == 8 || E == 16)) {
+    // configured path first; every miss (shape not instantiated, b too small)
+    // falls through to the square register tiles, then to the gather kernel
     const int path = tile_path(E, false);
-    if (path != 0) {
-      const int rc2 = dispatch_ring(path, E, q, false, src, dst, b, batch, src_batch_stride,
-                                    dst_batch_stride, st);
-      if (rc2 != BITREV_ETILE) return rc2;
+    if (path == 3) {
+      rc = dispatch_oop_rect(E, current_q(E, false), src, dst, b, batch, src_batch_stride,
+                             dst_batch_stride, st);
+      if (rc != BITREV_ETILE) return rc;
     }
-    return dispatch_oop_tile(E, q, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
+    for (int q = pick_q(E, b, false); q >= 3; --q) {
+      if (path == 1 || path == 2) {
+        rc = dispatch_ring(path, E, q, false, src, dst, b, batch, src_batch_stride,
+                           dst_batch_stride, st);
+        if (rc != BITREV_ETILE) return rc;
+      }
+      rc = dispatch_oop_tile(E, q, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
+      if (rc != BITREV_ETILE) return rc;
+    }
   }
   return dispatch_gather(E, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
 }
@@ -489,16 +608,17 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
   if (batch == 1) batch_stride = n;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (n * E <= kSmallBytes) return dispatch_small(E, a, a, b, batch, batch_stride, batch_stride, st);
-  const int q = pick_q(E, b, true);
   const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
-  if (q && vec_ok) {
+  if (vec_ok && (E == 4 || E == 8 || E == 16)) {
     const int path = tile_path(E, true);
-    if (path != 0) {
-      const int rc2 = dispatch_ring(path, E, q, true, a, a, b, batch, batch_stride, batch_stride,
-                                    st);
-      if (rc2 != BITREV_ETILE) return rc2;
+    for (int q = pick_q(E, b, true); q >= 3; --q) {
+      if (path == 1 || path == 2) {
+        rc = dispatch_ring(path, E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
+        if (rc != BITREV_ETILE) return rc;
+      }
+      rc = dispatch_ip_tile(E, q, a, b, batch, batch_stride, st);
+      if (rc != BITREV_ETILE) return rc;
     }
-    return dispatch_ip_tile(E, q, a, b, batch, batch_stride, st);
   }
   return dispatch_swap(E, a, b, batch, batch_stride, st);
 }
@@ -681,7 +801,7 @@ int bitrev_get_tile_path(int elem_bytes, int inplace) { return tile_path(elem_by
 
 int bitrev_set_tile_path(int elem_bytes, int inplace, int path) {
   if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16) return BITREV_ETILE;
-  if (path < 0 || path > 2) return BITREV_ETILE;
+  if (path < 0 || path > 3 || (path == 3 && inplace)) return BITREV_ETILE;
   (inplace ? g_path_ip : g_path_oop)[elem_bytes].store(path);
   return BITREV_OK;
 }
@@ -689,7 +809,7 @@ int bitrev_set_tile_path(int elem_bytes, int inplace, int path) {
 int bitrev_get_tile_order(int inplace) { return tile_order(inplace != 0); }
 
 int bitrev_set_tile_order(int inplace, int order) {
-  if (order < 0 || (order > 1 && (order & ~0x1ff) != 0) || (order > 1 && order < 0x100))
+  if (order < 0 || (order > 2 && (order & ~0x1ff) != 0) || (order > 2 && order < 0x100))
     return BITREV_ETILE;
   (inplace ? g_order_ip : g_order_oop).store(order);
   return BITREV_OK;

@@ -43,6 +43,9 @@
 #ifndef BITREV_RING_BUDGET_KB
 #define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
 #endif
+#ifndef BITREV_EXPERIMENT_ROWPAD
+#define BITREV_EXPERIMENT_ROWPAD 0  // timing experiment only: bytes added to the row stride
+#endif
 #ifndef BITREV_MINB_IP
 #define BITREV_MINB_IP 1  // __launch_bounds__ min CTAs/SM, in-place tile kernel
 #endif
@@ -211,6 +214,29 @@ struct TileArgs {
   int64_t src_bstride; // bytes between batch rows
   int64_t dst_bstride;
   int order;           // 0: y = work index; 1: bit-interleaved (see work_to_y)
+  uint64_t npairs;     // in place, compact pair enumeration: pairs per row (else 0)
+  uint64_t step_b;     // compact mode: gridDim.x = step_b * npairs + step_w
+  uint64_t step_w;
+  int64_t batch;
+};
+
+// Walks the compact pair enumeration of all batch rows with stride
+// gridDim.x, without divisions in the loop.
+struct PairCursor {
+  uint64_t bi, w;
+  __device__ __forceinline__ void start(const TileArgs& a) {
+    bi = blockIdx.x / a.npairs;
+    w = blockIdx.x - bi * a.npairs;
+  }
+  __device__ __forceinline__ void next(const TileArgs& a) {
+    w += a.step_w;
+    bi += a.step_b;
+    if (w >= a.npairs) {
+      w -= a.npairs;
+      ++bi;
+    }
+  }
+  __device__ __forceinline__ bool valid(const TileArgs& a) const { return bi < (uint64_t)a.batch; }
 };
 
 // Gather the even bits of x into its low half (Morton decode).
@@ -255,6 +281,40 @@ __device__ __forceinline__ uint64_t work_to_y(uint64_t w, int m, int order) {
   return (hi << (m - H)) | (mid << L) | lo;
 }
 
+// Number of middle values y with y <= rev_m(y): the unordered tile pairs
+// {y, rev(y)} of one row, palindromes included.
+__host__ __device__ inline uint64_t pair_count(int m) {
+  return ((1ull << m) + (1ull << ((m + 1) / 2))) >> 1;
+}
+
+// w-th canonical pair representative y (y <= rev_m(y)), a bijection of
+// [0, pair_count(m)) -- the swap-schedule structure of _fill_pairs
+// (src/schedule.py:53-75) at tile granularity.  Level k (k < m/2) holds the
+// y whose outer k bit pairs mirror each other and whose pair k is
+// (y_{m-1-k}, y_k) = (0, 1): 2^(m-k-2) values laid out after levels < k;
+// the 2^ceil(m/2) palindromes come last.  Lets the in-place kernels visit
+// exactly one item per pair: no skipped items, equal work per CTA.
+__device__ __forceinline__ uint64_t pair_from_index(uint64_t w, int m) {
+  if (m == 0) return 0;
+  const int h = m >> 1;
+  const uint64_t Sh = (1ull << (m - 1)) - (1ull << (m - h - 1));
+  if (w < Sh) {
+    const int k = __clzll((~w) << (64 - (m - 1)));  // leading ones of w in m-1 bits
+    const uint64_t o = w - ((1ull << (m - 1)) - (1ull << (m - k - 1)));
+    const int ib = m - 2 * k - 2;
+    const uint64_t inner = o & ((1ull << ib) - 1);
+    const uint64_t outer = o >> ib;
+    return (inner << (k + 1)) | (1ull << k) | outer | (dev_rev(outer, k) << (m - k));
+  }
+  const uint64_t p = w - Sh;
+  const uint64_t outer = p & ((1ull << h) - 1);
+  uint64_t y = outer | (dev_rev(outer, h) << (m - h));
+  if (m & 1) y |= ((p >> h) & 1ull) << h;
+  return y;
+}
+
+
+
 // ---------------------------------------------------------------------------
 // out-of-place tile kernel (replaces _cobra_copy, src/permutations.py:225-249)
 
@@ -263,7 +323,7 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_OOP)
     bitrev_oop_tile_kernel(TileArgs a) {
   using T = Tile<E, Q>;
   extern __shared__ __align__(16) uint4 smem[];
-  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t row_stride = ((uint64_t)E << (a.b - Q)) + BITREV_EXPERIMENT_ROWPAD;
   const uint64_t mmask = (1ull << a.m) - 1;
   uint4 r[T::IPT][T::V];
 
@@ -289,6 +349,95 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_OOP)
 }
 
 // ---------------------------------------------------------------------------
+// rectangular out-of-place tile kernel
+//
+// Out of place there is no pairing constraint, so the split can be uneven:
+//   i = x * 2^(b-QX) + y * 2^QZ + z,  x < 2^QX, z < 2^QZ, y < 2^(b-QX-QZ)
+//   rev_b(i) = rev_QZ(z) * 2^(b-QZ) + rev_m(y) * 2^QX + rev_QX(x).
+// A tile is 2^QX source pieces of 2^QZ*E bytes (short: consecutive y are
+// adjacent, so CTAs running together still read long runs) and 2^QZ
+// destination rows of 2^QX*E bytes (long: the scattered side gets >= 1 KB
+// runs) -- with a tile 2^(QZ-QX) times smaller than a square one of the same
+// destination run length.
+
+template <int E, int QX, int QZ>
+struct Rect {
+  static constexpr int V = 16 / E;
+  static constexpr int LV = const_log2(V);
+  static constexpr int XS = 1 << QX, ZS = 1 << QZ;
+  static constexpr int GX = XS / V;          // row groups / destination chunks per row
+  static constexpr int CZ = ZS / V;          // 16-byte chunks per source piece
+  static constexpr int ITEMS = GX * CZ;      // load items (V loads each)
+  static constexpr int WCH = ZS * GX;        // 16-byte chunks per tile
+  static constexpr int THREADS = ITEMS < 256 ? ITEMS : 256;
+  static constexpr int IPT = ITEMS / THREADS;
+  static constexpr int WPT = WCH / THREADS;
+  static constexpr int BYTES = XS * ZS * E;
+  static_assert(E == 4 || E == 8 || E == 16, "rect tiles move 4/8/16-byte elements");
+  static_assert(GX >= 8 && CZ >= 8, "XOR swizzle needs >= 8 chunks on both sides");
+  static_assert(ITEMS % THREADS == 0 && WCH % THREADS == 0, "even split");
+};
+
+template <int E, int QX, int QZ>
+__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
+    bitrev_oop_rect_kernel(TileArgs a) {
+  using T = Rect<E, QX, QZ>;
+  extern __shared__ __align__(16) uint4 smem[];
+  const uint64_t src_row = (uint64_t)E << (a.b - QX);   // stride between source pieces
+  const uint64_t dst_row = (uint64_t)E << (a.b - QZ);   // stride between destination rows
+  const uint64_t mmask = (1ull << a.m) - 1;
+  uint4 r[T::IPT][T::V];
+
+  auto load = [&](uint64_t tt) {
+    const uint64_t bi = tt >> a.m, y = work_to_y(tt & mmask, a.m, a.order);
+    const char* base = a.src + bi * a.src_bstride + (y << QZ) * E;
+#pragma unroll
+    for (int it = 0; it < T::IPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int c = id % T::CZ, g = id / T::CZ;
+#pragma unroll
+      for (int k = 0; k < T::V; ++k)
+        r[it][k] = ld_stream(base + (uint64_t)(g + k * T::GX) * src_row + (uint64_t)c * 16);
+    }
+  };
+  // U[z][col]: ZS rows of GX chunks, chunk' = chunk ^ ((z >> LV) & 7)
+  auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
+
+  uint64_t t = blockIdx.x;
+  if (t >= a.ntiles) return;
+  load(t);
+  for (;;) {
+    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
+#pragma unroll
+    for (int it = 0; it < T::IPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int c = id % T::CZ, g = id / T::CZ;
+      const int col = (int)(__brev((unsigned)g) >> (32 - (QX - T::LV)));
+      smem[sidx(c * T::V, col)] = xpose<E, 0>(r[it]);
+      if constexpr (T::V > 1) smem[sidx(c * T::V + 1, col)] = xpose<E, 1>(r[it]);
+      if constexpr (T::V > 2) {
+        smem[sidx(c * T::V + 2, col)] = xpose<E, 2>(r[it]);
+        smem[sidx(c * T::V + 3, col)] = xpose<E, 3>(r[it]);
+      }
+    }
+    __syncthreads();
+    const uint64_t tn = t + gridDim.x;
+    if (tn < a.ntiles) load(tn);
+    char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
+#pragma unroll
+    for (int it = 0; it < T::WPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int col = id % T::GX, z = id / T::GX;
+      const uint64_t rz = __brev((unsigned)z) >> (32 - QZ);
+      st_vec(dbase + rz * dst_row + (uint64_t)col * 16, smem[sidx(z, col)]);
+    }
+    if (tn >= a.ntiles) break;
+    __syncthreads();
+    t = tn;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // in-place tile-pair kernel (replaces _cobra_swap, src/permutations.py:252-285)
 //
 // Work item y (per batch row) with y <= rev(y): load tile y and tile rev(y) into
@@ -299,54 +448,75 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_OOP)
 // two CTAs ever touch the same element and both tiles are resident before the
 // first write.
 
-template <int E, int Q>
+template <int E, int Q, bool COMPACT>
 __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
     bitrev_inplace_tile_kernel(TileArgs a) {
   using T = Tile<E, Q>;
   extern __shared__ __align__(16) uint4 smem[];
   uint4* U0 = smem;
   uint4* U1 = smem + T::WCH;
-  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t row_stride = ((uint64_t)E << (a.b - Q)) + BITREV_EXPERIMENT_ROWPAD;
   const uint64_t mmask = (1ull << a.m) - 1;
   uint4 r0[T::IPT][T::V], r1[T::IPT][T::V];
 
-  // next work item at or after tt with y <= rev(y)
   auto partner = [&](uint64_t y) {
     return BITREV_EXPERIMENT_CONTIG ? (y ^ 1ull) : dev_rev(y, a.m);
   };
-  auto advance = [&](uint64_t tt) {
-    while (tt < a.ntiles) {
-      const uint64_t y = work_to_y(tt & mmask, a.m, a.order);
-      if (partner(y) >= y) break;
+  // Work cursor: COMPACT walks the pair enumeration (one item per pair);
+  // otherwise every y is visited in `order` and items with rev(y) < y skipped.
+  PairCursor pc;
+  uint64_t tt = blockIdx.x;
+  auto skip_fwd = [&]() {
+    while (tt < a.ntiles && partner(work_to_y(tt & mmask, a.m, a.order)) <
+                                work_to_y(tt & mmask, a.m, a.order))
       tt += gridDim.x;
-    }
-    return tt;
   };
-  auto issue = [&](uint64_t tt) {
-    const uint64_t bi = tt >> a.m, y = work_to_y(tt & mmask, a.m, a.order),
-                   ry = partner(y);
+  auto cur_valid = [&]() { return COMPACT ? pc.valid(a) : tt < a.ntiles; };
+  auto cur_item = [&](uint64_t& bi, uint64_t& y) {
+    if constexpr (COMPACT) {
+      bi = pc.bi;
+      y = pair_from_index(pc.w, a.m);
+    } else {
+      bi = tt >> a.m;
+      y = work_to_y(tt & mmask, a.m, a.order);
+    }
+  };
+  auto cur_next = [&]() {
+    if constexpr (COMPACT) {
+      pc.next(a);
+    } else {
+      tt += gridDim.x;
+      skip_fwd();
+    }
+  };
+  auto issue = [&]() {
+    uint64_t bi, y;
+    cur_item(bi, y);
+    const uint64_t ry = partner(y);
     const char* base = a.src + bi * a.src_bstride;
     tile_load<E, Q, BITREV_IP_NC>(r0, base + (y << Q) * E, row_stride);
     if (ry != y) tile_load<E, Q, BITREV_IP_NC>(r1, base + (ry << Q) * E, row_stride);
   };
 
-  uint64_t t = advance(blockIdx.x);
-  if (t >= a.ntiles) return;
-  issue(t);
+  if constexpr (COMPACT) pc.start(a); else skip_fwd();
+  if (!cur_valid()) return;
+  issue();
   for (;;) {
-    const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order), ry = partner(y);
+    uint64_t bi, y;
+    cur_item(bi, y);
+    const uint64_t ry = partner(y);
     const bool pair = ry != y;
     tile_stage<E, Q>(r0, U0);
     if (pair) tile_stage<E, Q>(r1, U1);
     __syncthreads();
-    const uint64_t tn = advance(t + gridDim.x);
-    if (tn < a.ntiles) issue(tn);
+    cur_next();
+    const bool more = cur_valid();
+    if (more) issue();
     char* base = a.dst + bi * a.dst_bstride;
     tile_drain<E, Q>(U0, base + (ry << Q) * E, row_stride);
     if (pair) tile_drain<E, Q>(U1, base + (y << Q) * E, row_stride);
-    if (tn >= a.ntiles) break;
+    if (!more) break;
     __syncthreads();
-    t = tn;
   }
 }
 
@@ -497,7 +667,7 @@ __device__ __forceinline__ void ring_drain(uint32_t tile, char* dst_base, uint64
 // one item = the pair {y, rev(y)} with y <= rev(y); both tiles are staged
 // before either is drained, and the pair's regions are touched by no other
 // item, so the in-place hazard is confined to the item.
-template <int E, int Q, bool INPLACE, int MODE>
+template <int E, int Q, bool INPLACE, int MODE, bool COMPACT>
 __global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
     bitrev_ring_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a) {
   using R = Ring<E, Q, INPLACE, MODE>;
@@ -510,15 +680,36 @@ __global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
   const uint64_t mmask = (1ull << a.m) - 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  auto advance = [&](uint64_t tt) {
-    if constexpr (INPLACE) {
-      while (tt < a.ntiles) {
-        const uint64_t y = work_to_y(tt & mmask, a.m, a.order);
+  // work cursor (see bitrev_inplace_tile_kernel); each role keeps its own
+  struct Cursor {
+    PairCursor pc;
+    uint64_t tt;
+  };
+  auto skip_fwd = [&](uint64_t t) {
+    if constexpr (INPLACE && !COMPACT) {
+      while (t < a.ntiles) {
+        const uint64_t y = work_to_y(t & mmask, a.m, a.order);
         if (dev_rev(y, a.m) >= y) break;
-        tt += gridDim.x;
+        t += gridDim.x;
       }
     }
-    return tt;
+    return t;
+  };
+  auto c_start = [&](Cursor& c) {
+    if constexpr (COMPACT) c.pc.start(a); else c.tt = skip_fwd(blockIdx.x);
+  };
+  auto c_valid = [&](const Cursor& c) { return COMPACT ? c.pc.valid(a) : c.tt < a.ntiles; };
+  auto c_next = [&](Cursor& c) {
+    if constexpr (COMPACT) c.pc.next(a); else c.tt = skip_fwd(c.tt + gridDim.x);
+  };
+  auto c_item = [&](const Cursor& c, uint64_t& bi, uint64_t& y) {
+    if constexpr (COMPACT) {
+      bi = c.pc.bi;
+      y = pair_from_index(c.pc.w, a.m);
+    } else {
+      bi = c.tt >> a.m;
+      y = work_to_y(c.tt & mmask, a.m, a.order);
+    }
   };
 
   if (threadIdx.x == 0) {
@@ -532,11 +723,13 @@ __global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
 
   if (warp == R::NCW) {
     // ---- producer warp
-    uint64_t t = advance(blockIdx.x);
-    for (int i = 0; t < a.ntiles; ++i) {
+    Cursor c;
+    c_start(c);
+    for (int i = 0; c_valid(c); ++i) {
       const int s = i % R::NS;
       if (i >= R::NS) mbar_wait(empty + 8 * s, (uint32_t)(((i / R::NS) - 1) & 1));
-      const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
+      uint64_t bi, y;
+      c_item(c, bi, y);
       const uint64_t ry = dev_rev(y, a.m);
       const bool pair = INPLACE && ry != y;
       const uint32_t st = base + s * R::STAGE;
@@ -558,15 +751,17 @@ __global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
                      bar);
         }
       }
-      t = advance(t + gridDim.x);
+      c_next(c);
     }
   } else {
     // ---- consumer warps
-    uint64_t t = advance(blockIdx.x);
-    for (int i = 0; t < a.ntiles; ++i) {
+    Cursor c;
+    c_start(c);
+    for (int i = 0; c_valid(c); ++i) {
       const int s = i % R::NS;
       mbar_wait(full + 8 * s, (uint32_t)((i / R::NS) & 1));
-      const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
+      uint64_t bi, y;
+      c_item(c, bi, y);
       const uint64_t ry = dev_rev(y, a.m);
       const uint32_t st = base + s * R::STAGE;
       char* dbase = a.dst + bi * a.dst_bstride;
@@ -576,7 +771,7 @@ __global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
                                         lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + 8 * s);
-      t = advance(t + gridDim.x);
+      c_next(c);
     }
   }
 }

@@ -3,7 +3,8 @@
 The reference tunes COBRA's block width q per size by timing candidates and
 keeping the fastest mean (ties toward the smaller buffer).  Here the knobs are
 the shared-memory tile bits Q and the staging path (0 = register staging,
-1 = per-row cp.async.bulk ring, 2 = TMA tensor-map ring) of each kernel family;
+1 = per-row cp.async.bulk ring, 2 = TMA tensor-map ring, 3 = rectangular
+register tiles, out of place only) of each kernel family;
 the output never depends on them.  Candidates are timed in interleaved rounds
 (every candidate once per round) with CUDA events, so clock or box drift during
 the run hits all candidates alike.  Records use the reference CSV schema
@@ -21,6 +22,8 @@ from .harness import BenchmarkRecord, make_record
 
 QS = {4: (5, 6, 7), 8: (4, 5, 6), 16: (3, 4, 5, 6)}
 PATHS = (0, 1, 2)
+# path 3: rectangular out-of-place tiles, q = destination-run bits QX
+RECT_QS = {4: (6, 7, 8), 8: (5, 6, 7), 16: (4, 5, 6, 7)}
 DTYPES = {4: torch.float32, 8: torch.float64, 16: torch.complex128}
 
 
@@ -42,9 +45,13 @@ def tune_tiles(elem_bytes: int, inplace: bool, b: int, candidates=None, rounds: 
         raise ValueError("tile kernels exist for 4, 8 and 16-byte elements")
     cands = list(candidates) if candidates is not None else [
         (q, p) for q in QS[elem_bytes] for p in PATHS if 2 * q <= b]
+    if candidates is None and not inplace:
+        cands += [(q, 3) for q in RECT_QS[elem_bytes] if q + 5 <= b]
     if not cands:
         raise ValueError(f"no candidate tile widths for b={b}")
-    bad = [q for q, _ in cands if 2 * q > b or q not in QS[elem_bytes]]
+    bad = [q for q, p in cands
+           if (p == 3 and (inplace or q not in RECT_QS[elem_bytes]))
+           or (p != 3 and (2 * q > b or q not in QS[elem_bytes]))]
     if bad:
         raise ValueError(f"candidates {bad} are not valid tile bits for b={b}")
     dev = torch.device(device) if device is not None else _core.require_cuda()

@@ -76,7 +76,7 @@ def test_every_tile_size(cuda, E, b):
     paths = [br.get_tile_path(E, False), br.get_tile_path(E, True)]
     try:
         for q in qs:
-            for order in (0, 1):
+            for order in (0, 1, 2):
                 for path in (0, 1, 2):
                     for inplace in (False, True):
                         br.set_tile_bits(E, inplace, q)
@@ -96,16 +96,41 @@ def test_every_tile_size(cuda, E, b):
             br.set_tile_path(E, inplace, paths[int(inplace)])
 
 
+@pytest.mark.parametrize("E,q", [(4, 6), (4, 7), (4, 8), (8, 5), (8, 6), (8, 7),
+                                 (16, 4), (16, 5), (16, 6), (16, 7)])
+@pytest.mark.parametrize("b,batch", [(12, 3), (13, 2), (17, 1), (21, 2)])
+def test_rect_out_of_place_tiles(cuda, E, q, b, batch):
+    """Rectangular out-of-place tiles (path 3), including widths below QX+QZ
+    (the dispatcher then falls back to square tiles)."""
+    host = rand_bits(1 << b, E, seed=7000 * E + 10 * b + q, batch=batch)
+    expected = orc.oracle_permute(host, b)
+    old = (br.get_tile_bits(E, False), br.get_tile_path(E, False))
+    try:
+        br.set_tile_bits(E, False, q)
+        br.set_tile_path(E, False, 3)
+        out = br.bitrev_batched(torch.from_numpy(host).to(cuda), b)
+        torch.cuda.synchronize()
+        assert_same(out, expected)
+    finally:
+        br.set_tile_bits(E, False, old[0])
+        br.set_tile_path(E, False, old[1])
+
+
+@pytest.mark.parametrize("order", [0, 2])
 @pytest.mark.parametrize("path", [0, 1, 2])
 @pytest.mark.parametrize("E", [4, 8, 16])
-@pytest.mark.parametrize("b,batch", [(14, 3), (15, 5), (19, 2), (22, 1)])
-def test_both_staging_paths(cuda, path, E, b, batch):
-    """Register-staged and TMA-bulk-staged tile kernels, batched rows, odd and
-    even widths, both families."""
+@pytest.mark.parametrize("b,batch", [(12, 2), (13, 3), (14, 3), (15, 5), (19, 2), (22, 1)])
+def test_both_staging_paths(cuda, order, path, E, b, batch):
+    """Register-staged and TMA-staged tile kernels, batched rows, odd and even
+    widths (middle widths m = 0, 1, ... included), both families, skip-order
+    and compact pair enumeration for the in-place kernels."""
     host = rand_bits(1 << b, E, seed=6000 * E + b, batch=batch)
     expected = orc.oracle_permute(host, b)
     old = (br.get_tile_path(E, False), br.get_tile_path(E, True))
+    old_order = (br.get_tile_order(False), br.get_tile_order(True))
     try:
+        br.set_tile_order(False, order)
+        br.set_tile_order(True, order)
         br.set_tile_path(E, False, path)
         br.set_tile_path(E, True, path)
         src = torch.from_numpy(host).to(cuda)
@@ -117,6 +142,8 @@ def test_both_staging_paths(cuda, path, E, b, batch):
     finally:
         br.set_tile_path(E, False, old[0])
         br.set_tile_path(E, True, old[1])
+        br.set_tile_order(False, old_order[0])
+        br.set_tile_order(True, old_order[1])
 
 
 @pytest.mark.parametrize("E", [4, 8, 16])
