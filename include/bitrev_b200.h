@@ -93,6 +93,22 @@ int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void
                         void* stream);
 
 /*
+ * Stream `count` independent host arrays (each `batch` rows of 2^b elements)
+ * through the GPU with the transfers overlapped: while array k is copied
+ * host->device, array k-1 is permuted and array k-2 copied back, on three
+ * internal streams (copy-in, compute, copy-out) over three device slots.
+ * PCIe is full duplex, so with pinned host memory the per-array time tends
+ * to max(H2D, D2H) instead of their sum.  host_dst[k] may equal host_src[k]
+ * (in place on the host), and a host array may recur in the sequence: a copy
+ * in waits for any in-flight copy out to the same host memory.  Ordered after prior work on `stream`; synchronous.
+ * dev_scratch: NULL (stream-ordered allocation) or 3 * batch * 2^b *
+ * elem_bytes bytes.  No reference counterpart: the extension a caller with
+ * many host arrays (the FFT pre-pass of BASELINE config 4) needs.
+ */
+int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int64_t count, int b,
+                         int elem_bytes, int64_t batch, void* dev_scratch, void* stream);
+
+/*
  * Square in-place transpose of the 2^h x 2^h row-major matrix at a
  * (`batch` matrices, batch_stride elements apart).
  * Replaces: transpose_square_inplace -> _transpose_diag/_transpose_offdiag

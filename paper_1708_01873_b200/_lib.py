@@ -27,6 +27,7 @@ SIGNATURES = {
     "bitrev_inplace": (_c_int, [_vp, _c_int, _c_int, _c_i64, _c_i64, _vp]),
     "bitrev_oop_host": (_c_int, [_vp, _vp, _c_int, _c_int, _c_i64, _vp, _vp, _vp]),
     "bitrev_inplace_host": (_c_int, [_vp, _c_int, _c_int, _c_i64, _vp, _vp]),
+    "bitrev_host_pipeline": (_c_int, [_vp, _vp, _c_i64, _c_int, _c_int, _c_i64, _vp, _vp]),
     "bitrev_transpose_square": (_c_int, [_vp, _c_int, _c_int, _c_i64, _c_i64, _vp]),
     "bitrev_even_odd": (_c_int, [_vp, _vp, _c_int, _c_int, _c_i64, _c_i64, _c_i64, _vp]),
     "bitrev_apply_pairs": (_c_int, [_vp, _vp, _c_i64, _c_int, _vp]),

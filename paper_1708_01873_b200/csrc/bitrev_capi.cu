@@ -526,11 +526,20 @@ int check_common(int b, int E, int64_t batch) {
   return BITREV_OK;
 }
 
-// Tile bits for (E, b): the configured q, reduced so that 2q <= b (the
-// dispatchers then walk further down to the largest instantiated width).
-int pick_q(int E, int b, bool inplace) {
+int min_square_q(int E) { return E == 16 ? 3 : (E == 8 ? 4 : 5); }
+
+// Tile bits for (E, b, batch): the configured q, reduced so that 2q <= b and
+// -- for small problems -- until there are >= 8 tiles per SM to spread over
+// the grid (a 2^20-element array has only 256 Q=6 tiles for 148 SMs).  The
+// dispatchers then walk further down to the largest instantiated width.
+int pick_q(int E, int b, bool inplace, int64_t batch) {
   int q = current_q(E, inplace);
   while (q > 0 && 2 * q > b) --q;
+  static const int shrink = env_int("BITREV_B200_SHRINK", 0);  // measured: no gain (launch floor)
+  if (shrink) {
+    const uint64_t want = 8ull * (uint64_t)device_sms();
+    while (q > min_square_q(E) && ((uint64_t)batch << (b - 2 * q)) < want) --q;
+  }
   return q;
 }
 
@@ -584,7 +593,7 @@ int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
                              dst_batch_stride, st);
       if (rc != BITREV_ETILE) return rc;
     }
-    for (int q = pick_q(E, b, false); q >= 3; --q) {
+    for (int q = pick_q(E, b, false, batch); q >= 3; --q) {
       if (path == 1 || path == 2) {
         rc = dispatch_ring(path, E, q, false, src, dst, b, batch, src_batch_stride,
                            dst_batch_stride, st);
@@ -611,7 +620,7 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
   const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
   if (vec_ok && (E == 4 || E == 8 || E == 16)) {
     const int path = tile_path(E, true);
-    for (int q = pick_q(E, b, true); q >= 3; --q) {
+    for (int q = pick_q(E, b, true, batch); q >= 3; --q) {
       if (path == 1 || path == 2) {
         rc = dispatch_ring(path, E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
         if (rc != BITREV_ETILE) return rc;
@@ -683,6 +692,94 @@ int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void
   e = cudaStreamSynchronize(st);
   if (rc == BITREV_OK && e != cudaSuccess) rc = (int)e;
   return rc;
+}
+
+int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int64_t count, int b,
+                         int elem_bytes, int64_t batch, void* dev_scratch, void* stream) {
+  int rc = check_common(b, elem_bytes, batch);
+  if (rc) return rc;
+  if (count < 0) return BITREV_EBATCH;
+  if (count == 0) return BITREV_OK;
+  if (!host_src || !host_dst) return BITREV_ENULL;
+  for (int64_t k = 0; k < count; ++k)
+    if (!host_src[k] || !host_dst[k]) return BITREV_ENULL;
+  constexpr int kSlots = 3;
+  const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
+  const int64_t n = int64_t(1) << b;
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  cudaStream_t sin = nullptr, sk = nullptr, sout = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[kSlots] = {}, ev_k[kSlots] = {}, ev_out[kSlots] = {};
+  void* own = nullptr;
+  char* slots = static_cast<char*>(dev_scratch);
+  cudaError_t e = cudaSuccess;
+#define PIPE_TRY(x)              \
+  do {                           \
+    e = (x);                     \
+    if (e != cudaSuccess) goto done; \
+  } while (0)
+  PIPE_TRY(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+  PIPE_TRY(cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking));
+  PIPE_TRY(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+  PIPE_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  for (int i = 0; i < kSlots; ++i) {
+    PIPE_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+    PIPE_TRY(cudaEventCreateWithFlags(&ev_k[i], cudaEventDisableTiming));
+    PIPE_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
+  }
+  // order after the caller's prior work
+  PIPE_TRY(cudaEventRecord(ev_start, user));
+  PIPE_TRY(cudaStreamWaitEvent(sin, ev_start, 0));
+  if (!slots) {
+    PIPE_TRY(cudaMallocAsync(&own, kSlots * bytes, sin));
+    slots = static_cast<char*>(own);
+  }
+  for (int64_t k = 0; k < count; ++k) {
+    const int s = (int)(k % kSlots);
+    char* buf = slots + (size_t)s * bytes;
+    if (k >= kSlots) PIPE_TRY(cudaStreamWaitEvent(sin, ev_out[s], 0));  // slot drained
+    // the host source may be the destination of a step still in flight
+    for (int64_t j = k - 1; j >= 0 && j > k - kSlots; --j) {
+      const uintptr_t a0 = (uintptr_t)host_src[k], d0 = (uintptr_t)host_dst[j];
+      if (a0 < d0 + bytes && d0 < a0 + bytes)
+        PIPE_TRY(cudaStreamWaitEvent(sin, ev_out[j % kSlots], 0));
+    }
+    PIPE_TRY(cudaMemcpyAsync(buf, host_src[k], bytes, cudaMemcpyHostToDevice, sin));
+    PIPE_TRY(cudaEventRecord(ev_in[s], sin));
+    PIPE_TRY(cudaStreamWaitEvent(sk, ev_in[s], 0));
+    rc = bitrev_inplace(buf, b, elem_bytes, batch, n, sk);
+    if (rc != BITREV_OK) goto done;
+    PIPE_TRY(cudaEventRecord(ev_k[s], sk));
+    PIPE_TRY(cudaStreamWaitEvent(sout, ev_k[s], 0));
+    PIPE_TRY(cudaMemcpyAsync(host_dst[k], buf, bytes, cudaMemcpyDeviceToHost, sout));
+    PIPE_TRY(cudaEventRecord(ev_out[s], sout));
+  }
+  if (own) {
+    // the allocation's last users are on sout
+    PIPE_TRY(cudaStreamWaitEvent(sin, ev_out[(count - 1) % kSlots], 0));
+    PIPE_TRY(cudaFreeAsync(own, sout));
+    own = nullptr;
+  }
+  PIPE_TRY(cudaStreamSynchronize(sout));
+done:
+#undef PIPE_TRY
+  if (own) {
+    cudaStreamSynchronize(sin);
+    cudaFree(own);
+  }
+  if (sin) cudaStreamSynchronize(sin);
+  if (sk) cudaStreamSynchronize(sk);
+  if (sout) cudaStreamSynchronize(sout);
+  for (int i = 0; i < kSlots; ++i) {
+    if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+    if (ev_k[i]) cudaEventDestroy(ev_k[i]);
+    if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+  }
+  if (ev_start) cudaEventDestroy(ev_start);
+  if (sin) cudaStreamDestroy(sin);
+  if (sk) cudaStreamDestroy(sk);
+  if (sout) cudaStreamDestroy(sout);
+  if (rc != BITREV_OK) return rc;
+  return e == cudaSuccess ? BITREV_OK : (int)e;
 }
 
 int bitrev_transpose_square(void* a, int h, int elem_bytes, int64_t batch, int64_t batch_stride,

@@ -40,3 +40,27 @@ def test_stub_reports_errors(lib):
     x = np.zeros(16, dtype=np.float64)
     rc = lib.bitrev_inplace_host(x.ctypes.data, 60, 8, 1, None, None)
     assert rc < 0 and b"width" in lib.bitrev_strerror(rc)
+
+
+@pytest.mark.parametrize("E,dt", [(8, np.float64), (16, np.complex128), (4, np.float32)])
+@pytest.mark.parametrize("b,batch,count", [(14, 1, 5), (20, 1, 4), (12, 3, 7)])
+def test_host_pipeline(cuda, E, dt, b, batch, count):
+    import torch
+
+    import paper_1708_01873_b200 as br
+
+    rng = np.random.default_rng(b + 100 * E + count)
+    arrays = [rng.integers(0, 256, (1 << b) * E * batch, dtype=np.uint8).view(dt).reshape(
+        (batch, 1 << b) if batch > 1 else (1 << b,)) for _ in range(count)]
+    expected = [np.ascontiguousarray(orc.oracle_permute(a, b)) for a in arrays]
+    # out of place into numpy destinations
+    outs = [np.empty_like(a) for a in arrays]
+    br.bitrev_host_pipeline(arrays, b, outs)
+    for o, e in zip(outs, expected):
+        assert np.array_equal(o.view(np.uint8), e.view(np.uint8))
+    # in place on pinned torch tensors, with the same host array repeated
+    pinned = [torch.from_numpy(a.copy()).pin_memory() for a in arrays[:2]]
+    seq = [pinned[k % 2] for k in range(4)]
+    br.bitrev_host_pipeline(seq, b)  # each array permuted twice -> identity
+    for p, a in zip(pinned, arrays[:2]):
+        assert np.array_equal(p.numpy().view(np.uint8), a.view(np.uint8))
