@@ -69,6 +69,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo + --same-device only to test the "
+                         "multi-rank plumbing on one GPU)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="debug: every rank uses cuda:0 (replica workloads only)")
     ap.add_argument("--no-soak", action="store_true",
                     help="skip the 0.5 s clock soak (for profiler runs)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0,
@@ -166,8 +171,8 @@ class ClockSampler:
             rows = parse([r for r in self.rows
                           if self.marks.get("load0", t0) <= r[0] <= self.marks.get("load1", t1)])
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
-                    "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0, "window": "no nvidia-smi samples in the run"}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for _, _, f in rows:
@@ -297,8 +302,12 @@ def main():
 
     world, rank, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev_index = 0 if args.same_device else local
+        torch.cuda.set_device(dev_index)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", torch.cuda.current_device())
     b, dtname, E, inplace, batch, desc = WORKLOADS[args.workload]
     dtype = getattr(torch, dtname)
@@ -345,9 +354,11 @@ def main():
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    # clock soak: keep the GPU busy ~0.5 s so the sampler sees load clocks
+    # clock soak: keep the GPU busy >= 0.5 s and until nvidia-smi (slow to
+    # start) has delivered a few samples under load (bounded at 5 s)
     t_soak = time.monotonic()
-    while not args.no_soak and time.monotonic() - t_soak < 0.5:
+    while not args.no_soak and time.monotonic() - t_soak < 5.0 and (
+            time.monotonic() - t_soak < 0.5 or len(sampler.rows) < 3):
         for _ in range(8):
             if flush is not None:
                 flush.zero_()
@@ -375,7 +386,8 @@ def main():
     step_s = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
     rank_time = sum(step_s)
     if world > 1:
-        t = torch.tensor([rank_time], dtype=torch.float64, device=dev)
+        t = torch.tensor([rank_time], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         job_time = float(t.item())
     else:
