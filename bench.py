@@ -52,6 +52,9 @@ WORKLOADS = {
     "cfg3-16": (30, "complex128", 16, False, 1, "out-of-place bit reversal, n=2^30 complex128"),
     "cfg4": (16, "complex64", 8, False, 4096,
              "batched out-of-place bit reversal, 4096 x n=2^16 complex64 (FFT pre-pass)"),
+    "cfg4-fft6": (16, "complex64", 8, False, 4096,
+                  "batched FFT pre-pass, 4096 x n=2^16 complex64: bit reversal fused with the "
+                  "first 6 radix-2 DIT stages"),
     "cfg5": (32, "complex64", 8, False, 1,
              "n=2^32 complex64 sharded by top bits, local reversal + NCCL all-to-all + interleave"),
 }
@@ -313,7 +316,7 @@ def main():
     dtype = getattr(torch, dtname)
 
     # per-rank work
-    if args.workload == "cfg4":
+    if args.workload.startswith("cfg4"):
         rows = batch // world
         scaling = "strong"
         shape = (rows, 1 << b)
@@ -338,6 +341,12 @@ def main():
     if args.workload == "cfg5":
         def step():
             return sharded.sharded_bitrev(x, b)
+    elif args.workload == "cfg4-fft6":
+        n_rows = shape[0]
+
+        def step():
+            _lib.call("bitrev_dit_prepass", x.data_ptr(), y.data_ptr(), b, E, n_rows, 1 << b,
+                      1 << b, 6, 0, stream.cuda_stream)
     elif inplace:
         def step():
             _core.launch_inplace(x, b)
@@ -415,14 +424,19 @@ def main():
             br.bitrev_host_pipeline(srcs, b, dsts)
 
         def single_step():
-            if args.workload == "cfg4":
+            if args.workload == "cfg4-fft6":
+                br.bitrev_dit_prepass(hosts[0], b, 6, out=houts[0])
+            elif args.workload == "cfg4":
                 br.bitrev_batched(hosts[0], b, houts[0])
             elif inplace:
                 br.cobra_in_place(hosts[0], cfg, b)
             else:
                 br.cobra_out_of_place(hosts[0], houts[0], cfg, b)
 
-        for fn, n_steps, key in ((run_pipeline, reps, "pipe"), (single_step, 1, "single")):
+        plan = ((run_pipeline, reps, "pipe"), (single_step, 1, "single"))
+        if args.workload == "cfg4-fft6":  # the host pipeline runs the plain permutation
+            plan = ((single_step, 1, "single"),)
+        for fn, n_steps, key in plan:
             fn()  # warm (stream/pool creation, page-locking caches)
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
@@ -443,8 +457,11 @@ def main():
                 e2e = rec
             else:
                 rec["path"] = ("one blocking call per array on a pinned host tensor "
-                               "(cobra_in_place / cobra_out_of_place / bitrev_batched)")
+                               "(cobra_in_place / cobra_out_of_place / bitrev_batched / "
+                               "bitrev_dit_prepass)")
                 e2e_single = rec
+        if e2e is None:
+            e2e = e2e_single
     sampler.stop()
     clocks = sampler.summary(t_wall0, t_wall1)
 
@@ -470,6 +487,7 @@ def main():
             "workload": f"{args.workload}: {desc}", "b": b, "elem_bytes": E, "inplace": inplace,
             "batch": batch, "per_gpu_bytes_moved": bytes_local,
             "parallelism": {"cfg4": f"batch rows sharded over {world} GPUs",
+                            "cfg4-fft6": f"batch rows sharded over {world} GPUs",
                             "cfg5": f"top {world.bit_length() - 1} index bits over {world} GPUs"
                             }.get(args.workload, f"replicas only ({world} independent arrays)"),
             "l2": "L2 flushed (512 MiB write) before every step" if need_flush else
@@ -479,7 +497,8 @@ def main():
         "gelem_per_s": value / (2 * E),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "bitrev_inplace_tile_kernel" if inplace else "bitrev_oop_tile_kernel",
+                     "kernel": ("bitrev_fft_prepass_kernel" if args.workload == "cfg4-fft6" else
+                                "bitrev_inplace_tile_kernel" if inplace else "bitrev oop tile kernel"),
                      "algorithmic_bytes_per_launch": bytes_local, "peak_source": peak_src,
                      "frac_of_8TBs_spec": achieved / 8000.0},
         "e2e": e2e,

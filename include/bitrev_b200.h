@@ -46,6 +46,8 @@ extern "C" {
 #define BITREV_EOVERLAP (-5)  /* src/dst ranges overlap (src/permutations.py:305) */
 #define BITREV_ESHARD (-6)    /* sharded plan needs 1 <= 2g <= b_local + g       */
 #define BITREV_ETILE (-7)     /* tile-bits override not supported               */
+#define BITREV_ESTAGES (-8)   /* FFT pre-pass: unsupported number of stages      */
+#define BITREV_EALIGN (-9)    /* FFT pre-pass tiles: rows not 16-byte aligned    */
 
 /* Library version string, e.g. "bitrev_b200 0.1.0 sm_100a". */
 const char* bitrev_version(void);
@@ -133,6 +135,21 @@ int bitrev_even_odd(const void* src, void* dst, int b, int elem_bytes, int64_t b
  * caller-supplied pair list; a complete schedule takes bitrev_inplace instead.
  */
 int bitrev_apply_pairs(void* a, const void* pairs, int64_t npairs, int elem_bytes, void* stream);
+
+/*
+ * FFT pre-pass: dst = the first `stages` radix-2 decimation-in-time butterfly
+ * stages applied to bit-reversed src, per row (complex64: elem_bytes 8,
+ * complex128: 16; forward twiddles exp(-2 pi i k / 2^s), or conjugated when
+ * inverse != 0, no normalisation).  stages = 0 is the plain permutation;
+ * stages = b is a complete unnormalised radix-2 FFT.  Rows of n*E <= 32 KB
+ * take any stages <= b; larger rows fuse up to 6 stages into the tile drain
+ * (b >= 12; b >= 10 for <= 5 stages) at the permutation's HBM traffic.
+ * Serves the downstream step the reference's permutation exists for
+ * (SURVEY.md 8(f) f2).  No reference counterpart.
+ */
+int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
+                       int64_t src_batch_stride, int64_t dst_batch_stride, int stages,
+                       int inverse, void* stream);
 
 /*
  * Step 3 of the top-bit sharded plan (no reference counterpart: the reference

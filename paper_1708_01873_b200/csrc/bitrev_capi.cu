@@ -559,6 +559,8 @@ const char* bitrev_strerror(int code) {
     case BITREV_EOVERLAP: return "source and dest must not overlap";
     case BITREV_ESHARD: return "sharded plan needs 2g <= b (global width)";
     case BITREV_ETILE: return "tile bits not instantiated for this element size";
+    case BITREV_ESTAGES: return "stages must be in 0..b (fused tiles: at most 6, and b >= 2*Q)";
+    case BITREV_EALIGN: return "fused FFT tiles need 16-byte aligned rows";
   }
   if (code > 0) return cudaGetErrorString(static_cast<cudaError_t>(code));
   return "unknown bitrev error";
@@ -852,6 +854,75 @@ int bitrev_apply_pairs(void* a, const void* pairs, int64_t npairs, int elem_byte
 #undef AP_CASE
   }
   return BITREV_EELEM;
+}
+
+int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
+                       int64_t src_batch_stride, int64_t dst_batch_stride, int stages,
+                       int inverse, void* stream) {
+  const int E = elem_bytes;
+  int rc = check_common(b, E, batch);
+  if (rc) return rc;
+  if (E != 8 && E != 16) return BITREV_EELEM;
+  if (!src || !dst) return BITREV_ENULL;
+  const int64_t n = int64_t(1) << b;
+  if (batch > 1 && (src_batch_stride < n || dst_batch_stride < n)) return BITREV_EBATCH;
+  if (batch == 1) src_batch_stride = dst_batch_stride = n;
+  {
+    const uintptr_t s0 = (uintptr_t)src, d0 = (uintptr_t)dst;
+    const uintptr_t s1 = s0 + (uintptr_t)((batch - 1) * src_batch_stride + n) * E;
+    const uintptr_t d1 = d0 + (uintptr_t)((batch - 1) * dst_batch_stride + n) * E;
+    if (s0 < d1 && d0 < s1) return BITREV_EOVERLAP;
+  }
+  if (stages < 0 || stages > b) return BITREV_ESTAGES;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  FftArgs fa;
+  memset(&fa, 0, sizeof fa);
+  fa.stages = stages;
+  fa.inverse = inverse ? 1 : 0;
+  TileArgs& a = fa.t;
+  a.src = static_cast<const char*>(src);
+  a.dst = static_cast<char*>(dst);
+  a.b = b;
+  a.batch = batch;
+  a.src_bstride = src_batch_stride * E;
+  a.dst_bstride = dst_batch_stride * E;
+  if (n * E <= kSmallBytes) {
+    const int bytes = (int)(n * E);
+    const int grid = grid_for((uint64_t)batch, 8);
+    if (E == 8) {
+      cudaFuncSetAttribute(fft_prepass_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallBytes);
+      fft_prepass_small_kernel<8><<<grid, 256, bytes, st>>>(fa);
+    } else {
+      cudaFuncSetAttribute(fft_prepass_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallBytes);
+      fft_prepass_small_kernel<16><<<grid, 256, bytes, st>>>(fa);
+    }
+    return finish_launch();
+  }
+  if (stages > 6) return BITREV_ESTAGES;  // fused tiles carry at most Q = 6 stages
+  const int q = (b >= 12) ? 6 : 5;
+  if (stages > q || 2 * q > b) return BITREV_ESTAGES;
+  const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
+                      ((dst_batch_stride * E) % 16 == 0);
+  if (!vec_ok) return BITREV_EALIGN;
+  a.m = b - 2 * q;
+  a.ntiles = (uint64_t)batch << a.m;
+#define FFT_LAUNCH(E_, Q_)                                                                   \
+  {                                                                                          \
+    using T = Tile<E_, Q_>;                                                                  \
+    auto kern = bitrev_fft_prepass_kernel<E_, Q_>;                                           \
+    static int per_sm = [&] {                                                                \
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES);     \
+      return occupancy(kern, T::THREADS, T::BYTES);                                          \
+    }();                                                                                     \
+    kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                      \
+    return finish_launch();                                                                  \
+  }
+  if (E == 8 && q == 5) FFT_LAUNCH(8, 5)
+  if (E == 8 && q == 6) FFT_LAUNCH(8, 6)
+  if (E == 16 && q == 5) FFT_LAUNCH(16, 5)
+  if (E == 16 && q == 6) FFT_LAUNCH(16, 6)
+#undef FFT_LAUNCH
+  return BITREV_ETILE;
 }
 
 int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int elem_bytes,

@@ -777,6 +777,264 @@ __global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
 }
 
 // ---------------------------------------------------------------------------
+// FFT pre-pass: bit reversal fused with the first radix-2 DIT stages
+//
+// An iterative decimation-in-time FFT of length 2^b first bit-reverses its
+// input (the permutation exists for this), then runs b
+// butterfly stages; stage s combines elements 2^(s-1) apart inside aligned
+// blocks of 2^s with twiddles W_{2^s}^k, k < 2^(s-1).  Stages 1..Q therefore
+// stay inside aligned blocks of 2^Q outputs -- exactly one destination row of
+// a tile -- and their twiddles depend only on the position inside the row.
+// The drain below runs them on the row before storing it: lane l of a warp
+// holds row elements l (and l + 32 for Q = 6), stages 1..5 exchange through
+// __shfl_xor, stage 6 is lane-local.  HBM traffic stays 2*n*E.
+//
+// Complex element types: E = 8 (complex64, float math) and E = 16
+// (complex128, double math).  Twiddles W_{2^Q}^j = exp(-/+ 2 pi i j / 2^Q)
+// are computed once per CTA in double precision into shared memory.
+
+template <int E> struct Cplx;
+template <> struct Cplx<8> {
+  using T = float2;
+  using R = float;
+};
+template <> struct Cplx<16> {
+  using T = double2;
+  using R = double;
+};
+
+template <typename T>
+__device__ __forceinline__ T cmul(T a, T b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename T>
+__device__ __forceinline__ T cadd(T a, T b) { return {a.x + b.x, a.y + b.y}; }
+template <typename T>
+__device__ __forceinline__ T csub(T a, T b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ float2 shfl_xor_c(float2 v, int m) {
+  return {__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m)};
+}
+__device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
+  return {__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m)};
+}
+
+// Q = 6 drain with all of a warp's rows in flight at once (ILP across rows):
+// 64 destination rows, RPW per warp, two elements per lane and row.
+//   complex64:  lane holds x' = 2l, 2l+1 (one 16-byte chunk): stage 1 is
+//               lane-local, stages 2..6 pair lanes l ^ 2^(s-2);
+//   complex128: lane holds x' = l, l+32: stages 1..5 pair lanes l ^ 2^(s-1),
+//               stage 6 is lane-local.
+template <int E, int NWARPS, int RPW>
+__device__ __forceinline__ void fft_drain_q6_rows(const uint4* U, char* dbase, uint64_t row_stride,
+                                                  const typename Cplx<E>::T* tw, int stages,
+                                                  int zbase, int lane);
+
+#ifndef BITREV_FFT_ROWS_IN_FLIGHT
+#define BITREV_FFT_ROWS_IN_FLIGHT 4  // rows per warp transformed together (ILP vs registers)
+#endif
+
+template <int E, int NWARPS>
+__device__ __forceinline__ void fft_drain_q6(const uint4* U, char* dbase, uint64_t row_stride,
+                                             const typename Cplx<E>::T* tw, int stages, int warp,
+                                             int lane) {
+  constexpr int RPW_ALL = 64 / NWARPS;
+  constexpr int RB = RPW_ALL < BITREV_FFT_ROWS_IN_FLIGHT ? RPW_ALL : BITREV_FFT_ROWS_IN_FLIGHT;
+#pragma unroll 1
+  for (int r0 = 0; r0 < RPW_ALL; r0 += RB)
+    fft_drain_q6_rows<E, NWARPS, RB>(U, dbase, row_stride, tw, stages, warp + r0 * NWARPS, lane);
+}
+
+template <int E, int NWARPS, int RPW>
+__device__ __forceinline__ void fft_drain_q6_rows(const uint4* U, char* dbase, uint64_t row_stride,
+                                                  const typename Cplx<E>::T* tw, int stages,
+                                                  int zbase, int lane) {
+  using C = typename Cplx<E>::T;
+  constexpr int Q = 6;
+  C v[RPW][2];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int z = zbase + r * NWARPS;
+    if constexpr (E == 8) {
+      const uint4 c = U[swz<8, Q>(z, lane)];
+      v[r][0] = make_float2(__uint_as_float(c.x), __uint_as_float(c.y));
+      v[r][1] = make_float2(__uint_as_float(c.z), __uint_as_float(c.w));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const uint4 c = U[swz<16, Q>(z, lane + 32 * k)];
+        v[r][k] = make_double2(__hiloint2double(c.y, c.x), __hiloint2double(c.w, c.z));
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 1; s <= Q; ++s) {
+    if (s > stages) break;
+    const int half = 1 << (s - 1);
+    const bool local = (E == 8) ? (s == 1) : (s == Q);
+    if (local) {
+      // pair (k = 0, k = 1) inside the lane; top element index x'top
+      const int xtop = (E == 8) ? 2 * lane : lane;
+      const C w = tw[(xtop & (half - 1)) << (Q - s)];
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const C t1 = cmul(v[r][1], w);
+        v[r][1] = csub(v[r][0], t1);
+        v[r][0] = cadd(v[r][0], t1);
+      }
+    } else {
+      const int mask = (E == 8) ? (1 << (s - 2)) : (1 << (s - 1));
+      const bool bottom = lane & mask;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int xp = (E == 8) ? 2 * lane + k : lane + 32 * k;
+        const C w = tw[(xp & (half - 1)) << (Q - s)];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          const C p = shfl_xor_c(v[r][k], mask);
+          v[r][k] = bottom ? csub(p, cmul(v[r][k], w)) : cadd(v[r][k], cmul(p, w));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int z = zbase + r * NWARPS;
+    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - Q)) * row_stride;
+    if constexpr (E == 8) {
+      st_vec(drow + (uint64_t)lane * 16,
+             make_uint4(__float_as_uint(v[r][0].x), __float_as_uint(v[r][0].y),
+                        __float_as_uint(v[r][1].x), __float_as_uint(v[r][1].y)));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        st_vec(drow + (uint64_t)(lane + 32 * k) * 16,
+               make_uint4(__double2loint(v[r][k].x), __double2hiint(v[r][k].x),
+                          __double2loint(v[r][k].y), __double2hiint(v[r][k].y)));
+    }
+  }
+}
+
+struct FftArgs {
+  TileArgs t;
+  int stages;   // DIT stages fused (<= Q)
+  int inverse;  // 1: conjugate twiddles (unnormalised inverse transform)
+};
+
+template <int E, int Q>
+__global__ void __launch_bounds__(Tile<E, Q>::THREADS)
+    bitrev_fft_prepass_kernel(FftArgs fa) {
+  using T = Tile<E, Q>;
+  using C = typename Cplx<E>::T;
+  using Rl = typename Cplx<E>::R;
+  static_assert(E == 8 || E == 16, "complex64 / complex128 only");
+  static_assert(Q == 5 || Q == 6, "one or two elements per lane");
+  constexpr int S = 1 << Q;
+  constexpr int PER_LANE = S / 32;
+  constexpr int NWARPS = T::THREADS / 32;
+  extern __shared__ __align__(16) uint4 smem[];
+  __shared__ C tw[S / 2];
+  const TileArgs& a = fa.t;
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t mmask = (1ull << a.m) - 1;
+  for (int j = threadIdx.x; j < S / 2; j += blockDim.x) {
+    double sn, cs;
+    sincospi((fa.inverse ? 2.0 : -2.0) * j / S, &sn, &cs);
+    tw[j] = C{(Rl)cs, (Rl)sn};
+  }
+  uint4 r[T::IPT][T::V];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  uint64_t t = blockIdx.x;
+  if (t >= a.ntiles) return;
+  tile_load<E, Q, true>(r, a.src + (t >> a.m) * a.src_bstride + ((t & mmask) << Q) * E, row_stride);
+  for (;;) {
+    const uint64_t bi = t >> a.m, y = t & mmask;
+    tile_stage<E, Q>(r, smem);
+    __syncthreads();
+    const uint64_t tn = t + gridDim.x;
+    if (tn < a.ntiles)
+      tile_load<E, Q, true>(r, a.src + (tn >> a.m) * a.src_bstride + ((tn & mmask) << Q) * E,
+                            row_stride);
+    char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << Q) * E;
+    if constexpr (Q == 6) {
+      fft_drain_q6<E, NWARPS>(smem, dbase, row_stride, tw, fa.stages, warp, lane);
+    } else
+    // Q = 5: warp per destination row z, elements x' = lane in registers
+    for (int z = warp; z < S; z += NWARPS) {
+      C v[PER_LANE];
+#pragma unroll
+      for (int k = 0; k < PER_LANE; ++k) {
+        const int xp = lane + 32 * k;
+        const char* chunk = reinterpret_cast<const char*>(&smem[swz<E, Q>(z, xp / T::V)]);
+        v[k] = *reinterpret_cast<const C*>(chunk + (xp % T::V) * E);
+      }
+      const int s_lane = fa.stages < 5 ? fa.stages : 5;
+      for (int s = 1; s <= s_lane; ++s) {
+        const int half = 1 << (s - 1);
+        const C w = tw[(lane & (half - 1)) << (Q - s)];
+        const bool bottom = lane & half;
+#pragma unroll
+        for (int k = 0; k < PER_LANE; ++k) {
+          const C p = shfl_xor_c(v[k], half);
+          v[k] = bottom ? csub(p, cmul(v[k], w)) : cadd(v[k], cmul(p, w));
+        }
+      }
+      if constexpr (PER_LANE == 2) {
+        if (fa.stages >= 6) {  // x' and x' + 32 live in the same lane
+          const C t1 = cmul(v[1], tw[lane]);
+          v[1] = csub(v[0], t1);
+          v[0] = cadd(v[0], t1);
+        }
+      }
+      char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - Q)) * row_stride;
+#pragma unroll
+      for (int k = 0; k < PER_LANE; ++k)
+        *reinterpret_cast<C*>(drow + (uint64_t)(lane + 32 * k) * E) = v[k];
+    }
+    if (tn >= a.ntiles) break;
+    __syncthreads();
+    t = tn;
+  }
+}
+
+// Small rows (n*E <= 32 KB, any number of stages up to b, i.e. a full
+// radix-2 FFT): one CTA per row, bit-reversed load into shared memory, then
+// the stages with a barrier between them, then a coalesced store.
+template <int E>
+__global__ void __launch_bounds__(256) fft_prepass_small_kernel(FftArgs fa) {
+  using C = typename Cplx<E>::T;
+  using Rl = typename Cplx<E>::R;
+  extern __shared__ __align__(16) uint4 smem_f[];
+  C* buf = reinterpret_cast<C*>(smem_f);
+  const TileArgs& a = fa.t;
+  const int b = a.b;
+  const int n = 1 << b;
+  const double sign = fa.inverse ? 2.0 : -2.0;
+  for (int64_t row = blockIdx.x; row < a.batch; row += gridDim.x) {
+    const C* src = reinterpret_cast<const C*>(a.src + row * a.src_bstride);
+    C* dst = reinterpret_cast<C*>(a.dst + row * a.dst_bstride);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) buf[dev_rev((uint64_t)i, b)] = src[i];
+    __syncthreads();
+    for (int s = 1; s <= fa.stages; ++s) {
+      const int half = 1 << (s - 1);
+      for (int t = threadIdx.x; t < n / 2; t += blockDim.x) {
+        const int k = t & (half - 1);
+        const int i0 = ((t >> (s - 1)) << s) + k;
+        double sn, cs;
+        sincospi(sign * k / (2 * half), &sn, &cs);
+        const C w{(Rl)cs, (Rl)sn};
+        const C u = buf[i0], v = cmul(buf[i0 + half], w);
+        buf[i0] = cadd(u, v);
+        buf[i0 + half] = csub(u, v);
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = buf[i];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // whole-row-in-shared-memory kernel for small n (n*E <= kSmallBytes); one CTA
 // per batch row, grid-stride over rows.  Works in place (src == dst) because
 // every read of a row precedes the barrier and every write follows it.

@@ -1,0 +1,65 @@
+"""FFT pre-pass: the bit reversal fused with the first radix-2 DIT stages.
+
+The permutation is the first step of an iterative decimation-in-time FFT
+(PAPER.md:60-148).  Stages 1..Q of that FFT act inside aligned blocks of 2^Q
+outputs, which are exactly the destination rows of the tile kernels, so
+bitrev_dit_prepass runs them in the tile drain at the permutation's HBM
+traffic.  Rows of at most 32 KB take any number of
+stages, so stages = b gives a complete (unnormalised) radix-2 FFT.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _core, _lib
+from ._core import as_tensor
+from .bits import check_width
+
+_COMPLEX = {torch.complex64: 8, torch.complex128: 16}
+
+
+def bitrev_dit_prepass(x, b: int, stages: int, inverse: bool = False, out=None) -> torch.Tensor:
+    """Bit-reverse each row of x (complex64/complex128, [2^b] or [batch, 2^b])
+    and apply the first `stages` radix-2 DIT butterfly stages, with twiddles
+    exp(-2 pi i k / 2^s) (conjugated when inverse; no 1/n scaling).
+
+    Returns out (allocated like x when not given).  CUDA tensors run
+    asynchronously on the current stream; host tensors are staged through the
+    device.
+    """
+    t = as_tensor(x, "x")
+    check_width(b)
+    if t.dtype not in _COMPLEX:
+        raise ValueError(f"dtype {t.dtype} is not complex64/complex128")
+    if t.dim() not in (1, 2) or t.shape[-1] != (1 << b):
+        raise ValueError(f"x length {t.shape[-1]} does not match 2**{b}")
+    if not 0 <= stages <= b:
+        raise ValueError(f"stages must be in 0..{b}, got {stages}")
+    dst = torch.empty_like(t) if out is None else as_tensor(out, "out")
+    if dst.shape != t.shape or dst.dtype != t.dtype:
+        raise ValueError("out must match x in shape and dtype")
+    if _core.shares_memory(t, dst):
+        raise ValueError("x and out must not overlap")
+    if t.is_cuda:
+        src_d, dst_d = t.contiguous(), (dst if dst.is_contiguous() else torch.empty_like(t))
+        dev = t.device
+    else:
+        dev = _core.require_cuda()
+        src_d = t.contiguous().to(dev)
+        dst_d = torch.empty_like(src_d)
+    batch = 1 if t.dim() == 1 else t.shape[0]
+    n = 1 << b
+    with torch.cuda.device(dev):
+        _lib.call("bitrev_dit_prepass", src_d.data_ptr(), dst_d.data_ptr(), b, _COMPLEX[t.dtype],
+                  batch, n, n, stages, int(bool(inverse)), _core._stream_ptr(dev))
+    if dst_d is not dst:
+        dst.copy_(dst_d)
+    return dst
+
+
+def max_fused_stages(b: int, elem_bytes: int) -> int:
+    """Stages the fused path accepts for a row of 2^b elements."""
+    if (1 << b) * elem_bytes <= 32 * 1024:
+        return b
+    return 6 if b >= 12 else (5 if b >= 10 else 0)

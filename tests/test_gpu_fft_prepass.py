@@ -1,0 +1,105 @@
+"""FFT pre-pass (bit reversal fused with radix-2 DIT stages) vs a float64
+numpy restatement of the same stages, and vs np.fft for complete small FFTs.
+
+Tolerance: complex128 |err| <= 1e-12 * max|ref|; complex64 |err| <= 2e-6 *
+stages * max|ref| (float32 butterflies, twiddles rounded from float64)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1708_01873_b200 as br
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def dit_reference(x, b, stages, inverse=False):
+    y = np.ascontiguousarray(orc.oracle_permute(x.astype(np.complex128), b))
+    shape = y.shape
+    for s in range(1, stages + 1):
+        half = 1 << (s - 1)
+        w = np.exp((2j if inverse else -2j) * np.pi * np.arange(half) / (2 * half))
+        blk = y.reshape(-1, 2 * half)
+        u, v = blk[:, :half], blk[:, half:] * w
+        y = np.concatenate([u + v, u - v], axis=1).reshape(shape)
+    return y
+
+
+def check(got, ref, dtype, stages):
+    got = got.cpu().numpy().astype(np.complex128)
+    scale = max(np.abs(ref).max(), 1e-30)
+    tol = 1e-12 if dtype == torch.complex128 else 2e-6 * max(stages, 1)
+    err = np.abs(got - ref).max() / scale
+    assert err <= tol, f"max rel err {err:.3e} > {tol:.1e}"
+
+
+def rand_complex(shape, dtype, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    return x.astype(np.complex64 if dtype == torch.complex64 else np.complex128)
+
+
+@pytest.mark.parametrize("dtype", [torch.complex64, torch.complex128])
+@pytest.mark.parametrize("b,stages", [(10, 5), (12, 6), (14, 6), (16, 0), (16, 3), (20, 6),
+                                      (21, 5), (22, 6)])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_fused_stages_match_reference(cuda, dtype, b, stages, inverse):
+    if (1 << b) * (8 if dtype == torch.complex64 else 16) <= 32768 and b > 12:
+        pytest.skip("small-row path covered below")
+    x = rand_complex(1 << b, dtype, b * 10 + stages)
+    got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages, inverse=inverse)
+    check(got, dit_reference(x, b, stages, inverse), dtype, stages)
+
+
+@pytest.mark.parametrize("dtype", [torch.complex64, torch.complex128])
+@pytest.mark.parametrize("b", [1, 2, 5, 8, 11])
+def test_small_rows_full_fft(cuda, dtype, b):
+    if (1 << b) * (8 if dtype == torch.complex64 else 16) > 32768:
+        pytest.skip("row does not fit the small path")
+    x = rand_complex((3, 1 << b), dtype, b)
+    got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, b)
+    check(got, np.fft.fft(x.astype(np.complex128), axis=-1), dtype, b)
+    inv = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, b, inverse=True)
+    check(inv, np.fft.ifft(x.astype(np.complex128), axis=-1) * (1 << b), dtype, b)
+
+
+def test_zero_stages_is_the_permutation(cuda):
+    b = 18
+    x = torch.from_numpy(rand_complex(1 << b, torch.complex64, 1)).to(cuda)
+    got = br.bitrev_dit_prepass(x, b, 0)
+    assert torch.equal(got.view(torch.int64), br.oracle_permute(x, b).view(torch.int64))
+
+
+def test_batched_and_host_arrays(cuda):
+    b, stages = 16, 6
+    x = rand_complex((5, 1 << b), torch.complex128, 7)
+    got = br.bitrev_dit_prepass(x, b, stages)  # numpy in -> staged through the device
+    check(got, dit_reference(x, b, stages), torch.complex128, stages)
+
+
+def test_completes_to_torch_fft(cuda):
+    """prepass (6 fused stages) + the remaining DIT stages in torch == torch.fft.fft."""
+    b = 16
+    x = torch.from_numpy(rand_complex(1 << b, torch.complex128, 3)).to(cuda)
+    y = br.bitrev_dit_prepass(x, b, 6)
+    for s in range(7, b + 1):
+        half = 1 << (s - 1)
+        w = torch.exp(-2j * torch.pi * torch.arange(half, device=cuda, dtype=torch.float64)
+                      / (2 * half))
+        blk = y.view(-1, 2 * half)
+        u, v = blk[:, :half], blk[:, half:] * w
+        y = torch.cat([u + v, u - v], dim=1).reshape(-1)
+    ref = torch.fft.fft(x)
+    assert (y - ref).abs().max().item() <= 1e-9 * ref.abs().max().item()
+
+
+def test_validation(cuda):
+    x = torch.zeros(1 << 14, dtype=torch.float32, device=cuda)
+    with pytest.raises(ValueError, match="complex"):
+        br.bitrev_dit_prepass(x, 14, 2)
+    z = torch.zeros(1 << 14, dtype=torch.complex64, device=cuda)
+    with pytest.raises(ValueError, match="stages"):
+        br.bitrev_dit_prepass(z, 14, 15)
+    with pytest.raises(br.BitrevError):
+        br.bitrev_dit_prepass(z, 14, 9)  # fused tiles carry at most 6 stages
