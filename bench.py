@@ -200,8 +200,9 @@ def cpu_reference_step_fn(workload, threads):
     np_dt = {"float32": np.float32, "float64": np.float64, "complex64": np.complex64,
              "complex128": np.complex128}[dtname]
     rng = np.random.default_rng(0)
-    if workload == "cfg4":
-        # the reference has no batched API: rows over the threads;
+    if workload.startswith("cfg4"):
+        # the reference has no batched API (and no FFT stages for cfg4-fft6:
+        # its CPU path is the permutation alone): rows over the threads;
         # each step permutes a bounded block of rows
         rows = max(threads, 64)
         arr = rng.standard_normal((rows, 1 << b)).astype(np_dt)
@@ -256,7 +257,8 @@ def run_reference_arm(args):
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
                          "sample": sample,
                          "method": "parallel_semi_recursive_permute (C port of src/parallel.py)"
-                         if args.workload != "cfg4" else "cobra_in_place per row on a thread pool"},
+                         if not args.workload.startswith("cfg4")
+                         else "cobra_in_place per row on a thread pool"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -285,7 +287,7 @@ def cpu_baseline(workload, target_s):
     return {"value": nbytes * len(ts) / total / 1e9, "unit": "GB/s", "cores": threads,
             "kind": kind, "sample": f"{sample}, {len(ts)} steps",
             "method": "parallel_semi_recursive_permute (C port of src/parallel.py:95-156)"
-            if workload != "cfg4" else "cobra_in_place per row on a thread pool"}
+            if not workload.startswith("cfg4") else "cobra_in_place per row on a thread pool"}
 
 
 # ---------------------------------------------------------------------------
