@@ -40,6 +40,9 @@
 #ifndef BITREV_EXPERIMENT_CONTIG
 #define BITREV_EXPERIMENT_CONTIG 0  // timing experiment only: partner = y ^ 1 (WRONG output)
 #endif
+#ifndef BITREV_TILE_THREADS
+#define BITREV_TILE_THREADS 256  // threads per CTA of the register tile kernels
+#endif
 #ifndef BITREV_RING_BUDGET_KB
 #define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
 #endif
@@ -108,7 +111,7 @@ struct Tile {
   static constexpr int CH = S / V;           // 16-byte chunks per tile row
   static constexpr int ITEMS = CH * CH;      // load items (V loads each)
   static constexpr int WCH = S * CH;         // 16-byte chunks per tile
-  static constexpr int THREADS = ITEMS < 256 ? ITEMS : 256;
+  static constexpr int THREADS = ITEMS < BITREV_TILE_THREADS ? ITEMS : BITREV_TILE_THREADS;
   static constexpr int IPT = ITEMS / THREADS;  // load items per thread
   static constexpr int WPT = WCH / THREADS;    // drain chunks per thread
   static constexpr int BYTES = S * S * E;
