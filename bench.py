@@ -418,7 +418,7 @@ def main():
         hosts = [x.cpu().pin_memory() for _ in range(nhost)]
         houts = None if inplace else [torch.empty_like(h).pin_memory() for h in hosts]
         cfg = br.CobraConfig(6)
-        reps = max(3, min(args.steps, 12))
+        reps = max(3, min(args.steps, 32))
 
         def run_pipeline():
             srcs = [hosts[k % nhost] for k in range(reps)]
