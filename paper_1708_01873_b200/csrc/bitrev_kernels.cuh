@@ -830,89 +830,112 @@ __device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
 template <int E, int NWARPS, int RPW>
 __device__ __forceinline__ void fft_drain_q6_rows(const uint4* U, char* dbase, uint64_t row_stride,
                                                   const typename Cplx<E>::T* tw, int stages,
-                                                  int zbase, int lane);
+                                                  int zbase, int lane, bool inverse);
 
 #ifndef BITREV_FFT_ROWS_IN_FLIGHT
-#define BITREV_FFT_ROWS_IN_FLIGHT 4  // rows per warp transformed together (ILP vs registers)
+#define BITREV_FFT_ROWS_IN_FLIGHT 2  // row pairs per warp transformed together (ILP vs registers)
 #endif
 
 template <int E, int NWARPS>
 __device__ __forceinline__ void fft_drain_q6(const uint4* U, char* dbase, uint64_t row_stride,
                                              const typename Cplx<E>::T* tw, int stages, int warp,
-                                             int lane) {
-  constexpr int RPW_ALL = 64 / NWARPS;
-  constexpr int RB = RPW_ALL < BITREV_FFT_ROWS_IN_FLIGHT ? RPW_ALL : BITREV_FFT_ROWS_IN_FLIGHT;
+                                             int lane, bool inverse) {
+  // rows of this warp: warp + i * NWARPS, i < 64 / NWARPS, taken as pairs
+  constexpr int PAIRS = 64 / NWARPS / 2;
+  constexpr int RB = PAIRS < BITREV_FFT_ROWS_IN_FLIGHT ? PAIRS : BITREV_FFT_ROWS_IN_FLIGHT;
 #pragma unroll 1
-  for (int r0 = 0; r0 < RPW_ALL; r0 += RB)
-    fft_drain_q6_rows<E, NWARPS, RB>(U, dbase, row_stride, tw, stages, warp + r0 * NWARPS, lane);
+  for (int p0 = 0; p0 < PAIRS; p0 += RB)
+    fft_drain_q6_rows<E, NWARPS, RB>(U, dbase, row_stride, tw, stages, warp + 2 * p0 * NWARPS,
+                                     lane, inverse);
 }
 
+// One batch of RPW row PAIRS per warp: half-warp h of the warp holds row
+// z = zbase + (2r + h) * NWARPS, lane ll = lane & 15 holds its elements
+// x' = 4 ll + j (j < 4, two 16-byte chunks).  Stages 1 and 2 are lane-local
+// with trivial twiddles (W_2^0 = 1, W_4^1 = -/+ i); stages 3..6 exchange with
+// lane ll ^ 2^(s-3) inside the half-warp, one complex multiply per element,
+// branch-free (u + sign * t * w).
 template <int E, int NWARPS, int RPW>
 __device__ __forceinline__ void fft_drain_q6_rows(const uint4* U, char* dbase, uint64_t row_stride,
                                                   const typename Cplx<E>::T* tw, int stages,
-                                                  int zbase, int lane) {
+                                                  int zbase, int lane, bool inverse) {
   using C = typename Cplx<E>::T;
-  constexpr int Q = 6;
-  C v[RPW][2];
+  using Rl = typename Cplx<E>::R;
+  constexpr int Q = 6, V = 16 / E;
+  const int h = lane >> 4, ll = lane & 15;
+  C v[RPW][4];
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
-    const int z = zbase + r * NWARPS;
-    if constexpr (E == 8) {
-      const uint4 c = U[swz<8, Q>(z, lane)];
-      v[r][0] = make_float2(__uint_as_float(c.x), __uint_as_float(c.y));
-      v[r][1] = make_float2(__uint_as_float(c.z), __uint_as_float(c.w));
-    } else {
+    const int z = zbase + (2 * r + h) * NWARPS;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const uint4 c = U[swz<16, Q>(z, lane + 32 * k)];
-        v[r][k] = make_double2(__hiloint2double(c.y, c.x), __hiloint2double(c.w, c.z));
+    for (int c = 0; c < 4 / V; ++c) {  // chunks holding x' = 4 ll .. 4 ll + 3
+      const uint4 q = U[swz<E, Q>(z, (4 * ll) / V + c)];
+      if constexpr (E == 8) {
+        v[r][2 * c] = make_float2(__uint_as_float(q.x), __uint_as_float(q.y));
+        v[r][2 * c + 1] = make_float2(__uint_as_float(q.z), __uint_as_float(q.w));
+      } else {
+        v[r][c] = make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
       }
     }
   }
+  if (stages >= 1) {
 #pragma unroll
-  for (int s = 1; s <= Q; ++s) {
+    for (int r = 0; r < RPW; ++r) {
+      const C a0 = v[r][0], a1 = v[r][1], a2 = v[r][2], a3 = v[r][3];
+      v[r][0] = cadd(a0, a1);
+      v[r][1] = csub(a0, a1);
+      v[r][2] = cadd(a2, a3);
+      v[r][3] = csub(a2, a3);
+    }
+  }
+  if (stages >= 2) {
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const C a0 = v[r][0], a1 = v[r][1], a2 = v[r][2], a3 = v[r][3];
+      // t = a3 * W_4^1: forward -i -> (a3.y, -a3.x); inverse +i -> (-a3.y, a3.x)
+      const C t = inverse ? C{-a3.y, a3.x} : C{a3.y, -a3.x};
+      v[r][0] = cadd(a0, a2);
+      v[r][2] = csub(a0, a2);
+      v[r][1] = cadd(a1, t);
+      v[r][3] = csub(a1, t);
+    }
+  }
+#pragma unroll
+  for (int s = 3; s <= Q; ++s) {
     if (s > stages) break;
     const int half = 1 << (s - 1);
-    const bool local = (E == 8) ? (s == 1) : (s == Q);
-    if (local) {
-      // pair (k = 0, k = 1) inside the lane; top element index x'top
-      const int xtop = (E == 8) ? 2 * lane : lane;
-      const C w = tw[(xtop & (half - 1)) << (Q - s)];
+    const int mask = 1 << (s - 3);
+    const bool bottom = ll & mask;
+    const Rl sgn = bottom ? Rl(-1) : Rl(1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const C w = tw[((4 * ll + j) & (half - 1)) << (Q - s)];
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
-        const C t1 = cmul(v[r][1], w);
-        v[r][1] = csub(v[r][0], t1);
-        v[r][0] = cadd(v[r][0], t1);
-      }
-    } else {
-      const int mask = (E == 8) ? (1 << (s - 2)) : (1 << (s - 1));
-      const bool bottom = lane & mask;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int xp = (E == 8) ? 2 * lane + k : lane + 32 * k;
-        const C w = tw[(xp & (half - 1)) << (Q - s)];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-          const C p = shfl_xor_c(v[r][k], mask);
-          v[r][k] = bottom ? csub(p, cmul(v[r][k], w)) : cadd(v[r][k], cmul(p, w));
-        }
+        const C p = shfl_xor_c(v[r][j], mask);
+        const C u = bottom ? p : v[r][j];
+        const C m = cmul(bottom ? v[r][j] : p, w);
+        v[r][j] = C{u.x + sgn * m.x, u.y + sgn * m.y};
       }
     }
   }
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
-    const int z = zbase + r * NWARPS;
-    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - Q)) * row_stride;
+    const int z = zbase + (2 * r + h) * NWARPS;
+    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - Q)) * row_stride +
+                 (uint64_t)(4 * ll) * E;
     if constexpr (E == 8) {
-      st_vec(drow + (uint64_t)lane * 16,
-             make_uint4(__float_as_uint(v[r][0].x), __float_as_uint(v[r][0].y),
-                        __float_as_uint(v[r][1].x), __float_as_uint(v[r][1].y)));
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        st_vec(drow + c * 16,
+               make_uint4(__float_as_uint(v[r][2 * c].x), __float_as_uint(v[r][2 * c].y),
+                          __float_as_uint(v[r][2 * c + 1].x), __float_as_uint(v[r][2 * c + 1].y)));
     } else {
 #pragma unroll
-      for (int k = 0; k < 2; ++k)
-        st_vec(drow + (uint64_t)(lane + 32 * k) * 16,
-               make_uint4(__double2loint(v[r][k].x), __double2hiint(v[r][k].x),
-                          __double2loint(v[r][k].y), __double2hiint(v[r][k].y)));
+      for (int c = 0; c < 4; ++c)
+        st_vec(drow + c * 16,
+               make_uint4(__double2loint(v[r][c].x), __double2hiint(v[r][c].x),
+                          __double2loint(v[r][c].y), __double2hiint(v[r][c].y)));
     }
   }
 }
@@ -960,7 +983,7 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS)
                             row_stride);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << Q) * E;
     if constexpr (Q == 6) {
-      fft_drain_q6<E, NWARPS>(smem, dbase, row_stride, tw, fa.stages, warp, lane);
+      fft_drain_q6<E, NWARPS>(smem, dbase, row_stride, tw, fa.stages, warp, lane, fa.inverse);
     } else
     // Q = 5: warp per destination row z, elements x' = lane in registers
     for (int z = warp; z < S; z += NWARPS) {
