@@ -77,6 +77,12 @@ def parse():
                          "multi-rank plumbing on one GPU)")
     ap.add_argument("--same-device", action="store_true",
                     help="debug: every rank uses cuda:0 (replica workloads only)")
+    ap.add_argument("--tile-bits", type=int, default=0,
+                    help="override the library's tile bits Q for this workload (tuning)")
+    ap.add_argument("--tile-path", type=int, default=-1,
+                    help="override the staging path (0 reg, 1 bulk ring, 2 tensor ring, 3 rect)")
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="cfg5: sub-chunks per all-to-all (exchange/unpack overlap)")
     ap.add_argument("--no-soak", action="store_true",
                     help="skip the 0.5 s clock soak (for profiler runs)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0,
@@ -340,9 +346,13 @@ def main():
     y = None if inplace else torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
 
+    if args.tile_bits:
+        _lib.set_tile_bits(E, inplace, args.tile_bits)
+    if args.tile_path >= 0:
+        _lib.set_tile_path(E, inplace, args.tile_path)
     if args.workload == "cfg5":
         def step():
-            return sharded.sharded_bitrev(x, b)
+            return sharded.sharded_bitrev(x, b, chunks=args.chunks)
     elif args.workload == "cfg4-fft6":
         n_rows = shape[0]
 
@@ -495,6 +505,7 @@ def main():
             "l2": "L2 flushed (512 MiB write) before every step" if need_flush else
                   f"working set {bytes_local // 2 >> 20} MiB per side > L2, no flush",
             "tile_bits": _lib.get_tile_bits(E, inplace),
+            "tile_path": _lib.get_tile_path(E, inplace),
         },
         "gelem_per_s": value / (2 * E),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

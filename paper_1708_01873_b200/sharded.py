@@ -48,56 +48,84 @@ def _local_bitrev(shard: torch.Tensor, b_local: int) -> torch.Tensor:
     return out
 
 
-def _unpack(recv: torch.Tensor, b_local: int, g: int) -> torch.Tensor:
-    out = torch.empty_like(recv)
+def _unpack(recv: torch.Tensor, b_local: int, g: int, out: torch.Tensor) -> None:
+    """Step 3 into `out` (contiguous, recv-sized): out[k*G + rev_g(r)] = recv[r*C + k]."""
     with torch.cuda.device(recv.device):
         _lib.call("bitrev_sharded_unpack", recv.data_ptr(), out.data_ptr(), b_local, g,
                   _core.elem_bytes(recv), _core._stream_ptr(recv.device))
-    return out
 
 
-def _all_to_all(recv: torch.Tensor, send: torch.Tensor, group) -> None:
-    dist.all_to_all_single(recv, send, group=group)
+def _all_to_all(outs: list, ins: list, group):
+    """Async all-to-all of equal chunk lists; returns the work handle."""
+    return dist.all_to_all(outs, ins, group=group, async_op=True)
 
 
-def sharded_bitrev(local: torch.Tensor, b: int, group=None, *,
+def sharded_bitrev(local: torch.Tensor, b: int, group=None, *, chunks: int = 1,
                    local_permute: Callable | None = None,
                    unpack: Callable | None = None,
                    all_to_all: Callable | None = None) -> torch.Tensor:
     """Bit-reverse the global 2^b array whose rank-r shard is `local`.
 
-    Returns this rank's shard of the permuted array (a new tensor).  The three
-    step callables default to the CUDA kernels and NCCL; they are injectable
-    so the exchange logic can be exercised with gloo on CPU tensors in tests.
+    Returns this rank's shard of the permuted array (a new tensor).
+    chunks = K > 1 splits every destination chunk into K sub-chunks that are
+    exchanged as K asynchronous all-to-alls; sub-chunk c is interleaved (step
+    3) as soon as its exchange lands, while c+1.. are still on the wire.  The
+    output of step 3 for sub-chunk c is the contiguous slice
+    [c*C/K*G, (c+1)*C/K*G) of the local result, so no extra copies are made.
+    The step callables default to the CUDA kernels and NCCL; they are
+    injectable so the exchange logic can be exercised with gloo on CPU tensors.
     """
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     g = check_plan(b, world)
     b_local = b - g
     if local.dim() != 1 or local.shape[0] != (1 << b_local):
         raise ValueError(f"local shard length {local.shape[0]} does not match 2**{b_local}")
+    C = 1 << (b_local - g)
+    if chunks < 1 or chunks & (chunks - 1) or chunks > C:
+        raise ValueError(f"chunks must be a power of two in 1..{C}, got {chunks}")
     local_permute = local_permute or _local_bitrev
     unpack = unpack or _unpack
     all_to_all = all_to_all or _all_to_all
     staged = local_permute(local.contiguous(), b_local)
     if world == 1:
         return staged
-    recv = torch.empty_like(staged)
-    all_to_all(recv, staged, group)
-    return unpack(recv, b_local, g)
+    G = world
+    sub = C // chunks
+    kb = chunks.bit_length() - 1
+    recv = torch.empty_like(staged).view(chunks, G, sub)   # [sub-chunk][source rank][k]
+    out = torch.empty_like(staged)
+    works = []
+    for c in range(chunks):
+        ins = [staged[d * C + c * sub: d * C + (c + 1) * sub] for d in range(G)]
+        outs = [recv[c, r] for r in range(G)]
+        works.append(all_to_all(outs, ins, group))
+    for c in range(chunks):
+        if works[c] is not None:
+            works[c].wait()
+        unpack(recv[c].reshape(-1), b_local - kb, g, out[c * sub * G:(c + 1) * sub * G])
+    return out
 
 
-def emulate_sharded(global_array: torch.Tensor, b: int, world_size: int) -> list[torch.Tensor]:
+def emulate_sharded(global_array: torch.Tensor, b: int, world_size: int,
+                    chunks: int = 1) -> list[torch.Tensor]:
     """Run the three steps for `world_size` virtual ranks on ONE device, with
-    the exchange done by device copies.  Used to check the plan's kernels on a
-    single GPU; the real exchange is sharded_bitrev under torchrun."""
+    the exchange done by device copies (sub-chunked exactly like
+    sharded_bitrev).  Used to check the plan's kernels on a single GPU; the
+    real exchange is sharded_bitrev under torchrun."""
     g = check_plan(b, world_size)
     b_local = b - g
     S = 1 << b_local
     C = 1 << (b_local - g)
+    G = world_size
+    sub = C // chunks
+    kb = chunks.bit_length() - 1
     staged = [_local_bitrev(global_array[r * S:(r + 1) * S].contiguous(), b_local)
-              for r in range(world_size)]
+              for r in range(G)]
     outs = []
-    for d in range(world_size):
-        recv = torch.cat([staged[r][d * C:(d + 1) * C] for r in range(world_size)])
-        outs.append(_unpack(recv, b_local, g))
+    for d in range(G):
+        out = torch.empty_like(staged[0])
+        for c in range(chunks):
+            recv = torch.cat([staged[r][d * C + c * sub:d * C + (c + 1) * sub] for r in range(G)])
+            _unpack(recv, b_local - kb, g, out[c * sub * G:(c + 1) * sub * G])
+        outs.append(out)
     return outs

@@ -155,12 +155,12 @@ def test_complex128_large_sampled_vs_cpu_oracle(cuda, b):
     assert torch.equal(out.view(torch.int64), x.view(torch.int64))
 
 
-@pytest.mark.parametrize("b,G,dtype", [(12, 2, torch.int64), (16, 4, torch.complex64),
-                                       (20, 8, torch.float32), (21, 8, torch.complex128),
-                                       (26, 8, torch.complex64)])
-def test_sharded_plan_kernels(cuda, b, G, dtype):
+@pytest.mark.parametrize("b,G,dtype,chunks", [(12, 2, torch.int64, 1), (16, 4, torch.complex64, 1),
+                                              (20, 8, torch.float32, 4), (21, 8, torch.complex128, 2),
+                                              (26, 8, torch.complex64, 8), (14, 2, torch.int32, 16)])
+def test_sharded_plan_kernels(cuda, b, G, dtype, chunks):
     x = torch.empty((1 << b) * torch.empty(0, dtype=dtype).element_size(), dtype=torch.uint8,
                     device=cuda).random_(0, 256).view(dtype)
-    outs = sharded.emulate_sharded(x, b, G)
+    outs = sharded.emulate_sharded(x, b, G, chunks)
     got = torch.cat(outs)
     assert torch.equal(got.view(torch.uint8), br.oracle_permute(x, b).view(torch.uint8))

@@ -65,7 +65,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, b, q):
+def _worker(rank, world, port, b, q, chunks=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -77,22 +77,44 @@ def _worker(rank, world, port, b, q):
         def local_permute(t, bits):
             return torch.from_numpy(orc.oracle_permute(t.numpy(), bits))
 
-        def unpack(recv, bits, gg):
-            return torch.from_numpy(unpack_np(recv.numpy(), bits, gg))
+        def unpack(recv, bits, gg, out):
+            out.copy_(torch.from_numpy(unpack_np(recv.numpy(), bits, gg)))
 
-        out = sharded.sharded_bitrev(local, b, local_permute=local_permute, unpack=unpack)
+        class _Done:
+            def __init__(self, reqs):
+                self.reqs = reqs
+
+            def wait(self):
+                for r in self.reqs:
+                    r.wait()
+
+        def all_to_all(outs, ins, group):
+            # gloo has no list all_to_all (NCCL does): point-to-point exchange
+            reqs = []
+            me = dist.get_rank()
+            for peer in range(dist.get_world_size()):
+                if peer == me:
+                    outs[peer].copy_(ins[peer])
+                    continue
+                reqs.append(dist.isend(ins[peer].contiguous(), peer))
+                reqs.append(dist.irecv(outs[peer], peer))
+            return _Done(reqs)
+
+        out = sharded.sharded_bitrev(local, b, chunks=chunks, local_permute=local_permute,
+                                     unpack=unpack, all_to_all=all_to_all)
         expect = orc.oracle_permute(full, b)[rank << bl:(rank + 1) << bl]
         q.put((rank, bool(np.array_equal(out.numpy(), expect))))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_bitrev_gloo(world):
+@pytest.mark.parametrize("world,chunks", [(2, 1), (4, 1), (2, 4), (4, 2)])
+def test_sharded_bitrev_gloo(world, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, 10, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 10, q, chunks))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=120) for _ in procs)
