@@ -52,9 +52,9 @@ WORKLOADS = {
     "cfg3-16": (30, "complex128", 16, False, 1, "out-of-place bit reversal, n=2^30 complex128"),
     "cfg4": (16, "complex64", 8, False, 4096,
              "batched out-of-place bit reversal, 4096 x n=2^16 complex64 (FFT pre-pass)"),
-    "cfg4-fft6": (16, "complex64", 8, False, 4096,
+    "cfg4-fft7": (16, "complex64", 8, False, 4096,
                   "batched FFT pre-pass, 4096 x n=2^16 complex64: bit reversal fused with the "
-                  "first 6 radix-2 DIT stages"),
+                  "first 7 radix-2 DIT stages"),
     "cfg5": (32, "complex64", 8, False, 1,
              "n=2^32 complex64 sharded by top bits, local reversal + NCCL all-to-all + interleave"),
 }
@@ -207,7 +207,7 @@ def cpu_reference_step_fn(workload, threads):
              "complex128": np.complex128}[dtname]
     rng = np.random.default_rng(0)
     if workload.startswith("cfg4"):
-        # the reference has no batched API (and no FFT stages for cfg4-fft6:
+        # the reference has no batched API (and no FFT stages for cfg4-fft7:
         # its CPU path is the permutation alone): rows over the threads;
         # each step permutes a bounded block of rows
         rows = max(threads, 64)
@@ -353,12 +353,12 @@ def main():
     if args.workload == "cfg5":
         def step():
             return sharded.sharded_bitrev(x, b, chunks=args.chunks)
-    elif args.workload == "cfg4-fft6":
+    elif args.workload == "cfg4-fft7":
         n_rows = shape[0]
 
         def step():
             _lib.call("bitrev_dit_prepass", x.data_ptr(), y.data_ptr(), b, E, n_rows, 1 << b,
-                      1 << b, 6, 0, stream.cuda_stream)
+                      1 << b, 7, 0, stream.cuda_stream)
     elif inplace:
         def step():
             _core.launch_inplace(x, b)
@@ -471,8 +471,8 @@ def main():
             br.bitrev_host_pipeline(srcs, b, dsts)
 
         def single_step():
-            if args.workload == "cfg4-fft6":
-                br.bitrev_dit_prepass(hosts[0], b, 6, out=houts[0])
+            if args.workload == "cfg4-fft7":
+                br.bitrev_dit_prepass(hosts[0], b, 7, out=houts[0])
             elif args.workload == "cfg4":
                 br.bitrev_batched(hosts[0], b, houts[0])
             elif inplace:
@@ -481,7 +481,7 @@ def main():
                 br.cobra_out_of_place(hosts[0], houts[0], cfg, b)
 
         plan = ((run_pipeline, reps, "pipe"), (single_step, 1, "single"))
-        if args.workload == "cfg4-fft6":  # the host pipeline runs the plain permutation
+        if args.workload == "cfg4-fft7":  # the host pipeline runs the plain permutation
             plan = ((single_step, 1, "single"),)
         for fn, n_steps, key in plan:
             fn()  # warm (stream/pool creation, page-locking caches)
@@ -534,7 +534,7 @@ def main():
             "workload": f"{args.workload}: {desc}", "b": b, "elem_bytes": E, "inplace": inplace,
             "batch": batch, "per_gpu_bytes_moved": bytes_local,
             "parallelism": {"cfg4": f"batch rows sharded over {world} GPUs",
-                            "cfg4-fft6": f"batch rows sharded over {world} GPUs",
+                            "cfg4-fft7": f"batch rows sharded over {world} GPUs",
                             "cfg5": f"top {world.bit_length() - 1} index bits over {world} GPUs"
                             }.get(args.workload, f"replicas only ({world} independent arrays)"),
             "l2": "L2 flushed before every step (512 MiB write, then a 256 MiB read so "
@@ -546,7 +546,7 @@ def main():
         "gelem_per_s": value / (2 * E),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("bitrev_fft_prepass_kernel" if args.workload == "cfg4-fft6" else
+                     "kernel": ("bitrev_fft_rect_kernel" if args.workload == "cfg4-fft7" else
                                 "bitrev_inplace_tile_kernel" if inplace else "bitrev oop tile kernel"),
                      "algorithmic_bytes_per_launch": bytes_local, "peak_source": peak_src,
                      "frac_of_8TBs_spec": achieved / 8000.0,

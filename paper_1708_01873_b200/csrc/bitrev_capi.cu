@@ -559,7 +559,7 @@ const char* bitrev_strerror(int code) {
     case BITREV_EOVERLAP: return "source and dest must not overlap";
     case BITREV_ESHARD: return "sharded plan needs 2g <= b (global width)";
     case BITREV_ETILE: return "tile bits not instantiated for this element size";
-    case BITREV_ESTAGES: return "stages must be in 0..b (fused tiles: at most 6, and b >= 2*Q)";
+    case BITREV_ESTAGES: return "stages must be in 0..b (fused tiles: at most 7 for complex64, 6 for complex128)";
     case BITREV_EALIGN: return "fused FFT tiles need 16-byte aligned rows";
   }
   if (code > 0) return cudaGetErrorString(static_cast<cudaError_t>(code));
@@ -898,18 +898,21 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     }
     return finish_launch();
   }
-  if (stages > 6) return BITREV_ESTAGES;  // fused tiles carry at most Q = 6 stages
-  const int q = (b >= 12) ? 6 : 5;
-  if (stages > q || 2 * q > b) return BITREV_ESTAGES;
+  // Fused path: rectangular tiles whose destination rows are the FFT blocks
+  // (complex64: QX = 7, 128-element rows, up to 7 stages; complex128: QX = 6,
+  // 64-element rows, up to 6 stages).  Rows too big for the small kernel are
+  // always wide enough (b >= 13 resp. 12 > QX + QZ).
+  const int qx = E == 8 ? 7 : 6, qz = E == 8 ? 4 : 3;
+  if (stages > qx || b < qx + qz) return BITREV_ESTAGES;
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
   if (!vec_ok) return BITREV_EALIGN;
-  a.m = b - 2 * q;
+  a.m = b - qx - qz;
   a.ntiles = (uint64_t)batch << a.m;
-#define FFT_LAUNCH(E_, Q_)                                                                   \
+#define FFT_LAUNCH(E_, QX_, QZ_)                                                             \
   {                                                                                          \
-    using T = Tile<E_, Q_>;                                                                  \
-    auto kern = bitrev_fft_prepass_kernel<E_, Q_>;                                           \
+    using T = Rect<E_, QX_, QZ_>;                                                            \
+    auto kern = bitrev_fft_rect_kernel<E_, QX_, QZ_>;                                        \
     static int per_sm = [&] {                                                                \
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES);     \
       return occupancy(kern, T::THREADS, T::BYTES);                                          \
@@ -917,10 +920,8 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                      \
     return finish_launch();                                                                  \
   }
-  if (E == 8 && q == 5) FFT_LAUNCH(8, 5)
-  if (E == 8 && q == 6) FFT_LAUNCH(8, 6)
-  if (E == 16 && q == 5) FFT_LAUNCH(16, 5)
-  if (E == 16 && q == 6) FFT_LAUNCH(16, 6)
+  if (E == 8) FFT_LAUNCH(8, 7, 4)
+  if (E == 16) FFT_LAUNCH(16, 6, 3)
 #undef FFT_LAUNCH
   return BITREV_ETILE;
 }

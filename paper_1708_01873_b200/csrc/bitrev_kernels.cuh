@@ -827,196 +827,173 @@ __device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
 //               lane-local, stages 2..6 pair lanes l ^ 2^(s-2);
 //   complex128: lane holds x' = l, l+32: stages 1..5 pair lanes l ^ 2^(s-1),
 //               stage 6 is lane-local.
-template <int E, int NWARPS, int RPW>
-__device__ __forceinline__ void fft_drain_q6_rows(const uint4* U, char* dbase, uint64_t row_stride,
-                                                  const typename Cplx<E>::T* tw, int stages,
-                                                  int zbase, int lane, bool inverse);
+struct FftArgs {
+  TileArgs t;
+  int stages;   // DIT stages fused (<= QX)
+  int inverse;  // 1: conjugate twiddles (unnormalised inverse transform)
+};
 
-#ifndef BITREV_FFT_ROWS_IN_FLIGHT
-#define BITREV_FFT_ROWS_IN_FLIGHT 2  // row pairs per warp transformed together (ILP vs registers)
-#endif
+// FFT on destination rows of 2^QX elements held in a rectangular tile's
+// shared buffer U[z][chunk] (Rect<E, QX, QZ> swizzle).  Lanes hold 4 adjacent
+// elements x' = 4 ll + j; LPR = 2^QX / 4 lanes per row (16 or 32), so a warp
+// transforms 32 / LPR rows per pass.  Stages 1 and 2 are lane-local with
+// trivial twiddles (1, -/+ i); stages 3..QX exchange with lane ll ^ 2^(s-3)
+// inside the row's lane group, one complex multiply per element,
+// branch-free (u + sign * t * w).  Twiddles W_{2^QX}^j come from `tw`.
+// Twiddles of stages 3..QX in shared memory, laid out per stage as
+// T_s[j][l'] = W_{2^s}^{4 l' + j} (l' < 2^(s-3)) at offset 2^(s-1) - 4: a lane
+// with l' = ll mod 2^(s-3) reads word l' of row j, so the lanes of a warp
+// read consecutive words (or broadcast) -- no bank conflicts, no registers.
+__host__ __device__ constexpr int tw_offset(int s) { return (1 << (s - 1)) - 4; }
 
-template <int E, int NWARPS>
-__device__ __forceinline__ void fft_drain_q6(const uint4* U, char* dbase, uint64_t row_stride,
-                                             const typename Cplx<E>::T* tw, int stages, int warp,
-                                             int lane, bool inverse) {
-  // rows of this warp: warp + i * NWARPS, i < 64 / NWARPS, taken as pairs
-  constexpr int PAIRS = 64 / NWARPS / 2;
-  constexpr int RB = PAIRS < BITREV_FFT_ROWS_IN_FLIGHT ? PAIRS : BITREV_FFT_ROWS_IN_FLIGHT;
-#pragma unroll 1
-  for (int p0 = 0; p0 < PAIRS; p0 += RB)
-    fft_drain_q6_rows<E, NWARPS, RB>(U, dbase, row_stride, tw, stages, warp + 2 * p0 * NWARPS,
-                                     lane, inverse);
-}
-
-// One batch of RPW row PAIRS per warp: half-warp h of the warp holds row
-// z = zbase + (2r + h) * NWARPS, lane ll = lane & 15 holds its elements
-// x' = 4 ll + j (j < 4, two 16-byte chunks).  Stages 1 and 2 are lane-local
-// with trivial twiddles (W_2^0 = 1, W_4^1 = -/+ i); stages 3..6 exchange with
-// lane ll ^ 2^(s-3) inside the half-warp, one complex multiply per element,
-// branch-free (u + sign * t * w).
-template <int E, int NWARPS, int RPW>
-__device__ __forceinline__ void fft_drain_q6_rows(const uint4* U, char* dbase, uint64_t row_stride,
-                                                  const typename Cplx<E>::T* tw, int stages,
-                                                  int zbase, int lane, bool inverse) {
+template <int E, int QX, int QZ>
+__device__ __forceinline__ void fft_rows_drain(const uint4* U, char* dbase, uint64_t dst_row,
+                                               const typename Cplx<E>::T* tw, int stages,
+                                               bool inverse) {
   using C = typename Cplx<E>::T;
   using Rl = typename Cplx<E>::R;
-  constexpr int Q = 6, V = 16 / E;
-  const int h = lane >> 4, ll = lane & 15;
-  C v[RPW][4];
+  using T = Rect<E, QX, QZ>;
+  constexpr int V = T::V, LPR = (1 << QX) / 4, RPP = 32 / LPR;  // rows per warp pass
+  constexpr int NWARPS = T::THREADS / 32;
+  constexpr int ROWS = 1 << QZ;
+  // all rows of a warp are transformed together (independent shuffle chains)
+  constexpr int NR = (ROWS + NWARPS * RPP - 1) / (NWARPS * RPP);
+  static_assert(LPR == 16 || LPR == 32, "rows of 64 or 128 elements");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp * RPP >= ROWS) return;  // warp-uniform: more warps than rows
+  const int h = lane / LPR, ll = lane % LPR;
+  auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
+  auto row_of = [&](int i) { return (warp + i * NWARPS) * RPP + h; };
+  C v[NR][4];
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int z = zbase + (2 * r + h) * NWARPS;
+  for (int i = 0; i < NR; ++i) {
+    const int z = row_of(i);
 #pragma unroll
-    for (int c = 0; c < 4 / V; ++c) {  // chunks holding x' = 4 ll .. 4 ll + 3
-      const uint4 q = U[swz<E, Q>(z, (4 * ll) / V + c)];
+    for (int c = 0; c < 4 / V; ++c) {
+      const uint4 q = U[sidx(z, (4 * ll) / V + c)];
       if constexpr (E == 8) {
-        v[r][2 * c] = make_float2(__uint_as_float(q.x), __uint_as_float(q.y));
-        v[r][2 * c + 1] = make_float2(__uint_as_float(q.z), __uint_as_float(q.w));
+        v[i][2 * c] = make_float2(__uint_as_float(q.x), __uint_as_float(q.y));
+        v[i][2 * c + 1] = make_float2(__uint_as_float(q.z), __uint_as_float(q.w));
       } else {
-        v[r][c] = make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
+        v[i][c] = make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
       }
     }
   }
   if (stages >= 1) {
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const C a0 = v[r][0], a1 = v[r][1], a2 = v[r][2], a3 = v[r][3];
-      v[r][0] = cadd(a0, a1);
-      v[r][1] = csub(a0, a1);
-      v[r][2] = cadd(a2, a3);
-      v[r][3] = csub(a2, a3);
+    for (int i = 0; i < NR; ++i) {
+      const C a0 = v[i][0], a1 = v[i][1], a2 = v[i][2], a3 = v[i][3];
+      v[i][0] = cadd(a0, a1);
+      v[i][1] = csub(a0, a1);
+      v[i][2] = cadd(a2, a3);
+      v[i][3] = csub(a2, a3);
     }
   }
   if (stages >= 2) {
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const C a0 = v[r][0], a1 = v[r][1], a2 = v[r][2], a3 = v[r][3];
-      // t = a3 * W_4^1: forward -i -> (a3.y, -a3.x); inverse +i -> (-a3.y, a3.x)
-      const C t = inverse ? C{-a3.y, a3.x} : C{a3.y, -a3.x};
-      v[r][0] = cadd(a0, a2);
-      v[r][2] = csub(a0, a2);
-      v[r][1] = cadd(a1, t);
-      v[r][3] = csub(a1, t);
+    for (int i = 0; i < NR; ++i) {
+      const C a0 = v[i][0], a1 = v[i][1], a2 = v[i][2], a3 = v[i][3];
+      const C t = inverse ? C{-a3.y, a3.x} : C{a3.y, -a3.x};  // a3 * W_4^1
+      v[i][0] = cadd(a0, a2);
+      v[i][2] = csub(a0, a2);
+      v[i][1] = cadd(a1, t);
+      v[i][3] = csub(a1, t);
     }
   }
 #pragma unroll
-  for (int s = 3; s <= Q; ++s) {
+  for (int s = 3; s <= QX; ++s) {
     if (s > stages) break;
     const int half = 1 << (s - 1);
     const int mask = 1 << (s - 3);
     const bool bottom = ll & mask;
     const Rl sgn = bottom ? Rl(-1) : Rl(1);
+    const int lp = ll & ((half >> 2) - 1);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const C w = tw[((4 * ll + j) & (half - 1)) << (Q - s)];
+      const C w = tw[tw_offset(s) + j * (half >> 2) + lp];
 #pragma unroll
-      for (int r = 0; r < RPW; ++r) {
-        const C p = shfl_xor_c(v[r][j], mask);
-        const C u = bottom ? p : v[r][j];
-        const C m = cmul(bottom ? v[r][j] : p, w);
-        v[r][j] = C{u.x + sgn * m.x, u.y + sgn * m.y};
+      for (int i = 0; i < NR; ++i) {
+        const C p = shfl_xor_c(v[i][j], mask);
+        const C u = bottom ? p : v[i][j];
+        const C m = cmul(bottom ? v[i][j] : p, w);
+        v[i][j] = C{u.x + sgn * m.x, u.y + sgn * m.y};
       }
     }
   }
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int z = zbase + (2 * r + h) * NWARPS;
-    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - Q)) * row_stride +
+  for (int i = 0; i < NR; ++i) {
+    const int z = row_of(i);
+    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - QZ)) * dst_row +
                  (uint64_t)(4 * ll) * E;
     if constexpr (E == 8) {
 #pragma unroll
       for (int c = 0; c < 2; ++c)
         st_vec(drow + c * 16,
-               make_uint4(__float_as_uint(v[r][2 * c].x), __float_as_uint(v[r][2 * c].y),
-                          __float_as_uint(v[r][2 * c + 1].x), __float_as_uint(v[r][2 * c + 1].y)));
+               make_uint4(__float_as_uint(v[i][2 * c].x), __float_as_uint(v[i][2 * c].y),
+                          __float_as_uint(v[i][2 * c + 1].x), __float_as_uint(v[i][2 * c + 1].y)));
     } else {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        st_vec(drow + c * 16,
-               make_uint4(__double2loint(v[r][c].x), __double2hiint(v[r][c].x),
-                          __double2loint(v[r][c].y), __double2hiint(v[r][c].y)));
+        st_vec(drow + c * 16, make_uint4(__double2loint(v[i][c].x), __double2hiint(v[i][c].x),
+                                         __double2loint(v[i][c].y), __double2hiint(v[i][c].y)));
     }
   }
 }
 
-struct FftArgs {
-  TileArgs t;
-  int stages;   // DIT stages fused (<= Q)
-  int inverse;  // 1: conjugate twiddles (unnormalised inverse transform)
-};
-
-template <int E, int Q>
-__global__ void __launch_bounds__(Tile<E, Q>::THREADS)
-    bitrev_fft_prepass_kernel(FftArgs fa) {
-  using T = Tile<E, Q>;
+// Rectangular-tile FFT pre-pass (bitrev_oop_rect_kernel's load/stage path).
+template <int E, int QX, int QZ>
+__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
+    bitrev_fft_rect_kernel(FftArgs fa) {
+  using T = Rect<E, QX, QZ>;
   using C = typename Cplx<E>::T;
   using Rl = typename Cplx<E>::R;
-  static_assert(E == 8 || E == 16, "complex64 / complex128 only");
-  static_assert(Q == 5 || Q == 6, "one or two elements per lane");
-  constexpr int S = 1 << Q;
-  constexpr int PER_LANE = S / 32;
-  constexpr int NWARPS = T::THREADS / 32;
   extern __shared__ __align__(16) uint4 smem[];
-  __shared__ C tw[S / 2];
+  __shared__ C tw[(1 << QX) - 4];
   const TileArgs& a = fa.t;
-  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t src_row = (uint64_t)E << (a.b - QX);
+  const uint64_t dst_row = (uint64_t)E << (a.b - QZ);
   const uint64_t mmask = (1ull << a.m) - 1;
-  for (int j = threadIdx.x; j < S / 2; j += blockDim.x) {
+  for (int e = threadIdx.x; e < (1 << QX) - 4; e += blockDim.x) {
+    int s = 3;
+    while (e >= tw_offset(s + 1)) ++s;  // stage of table entry e
+    const int q = 1 << (s - 3), j = (e - tw_offset(s)) / q, lp = (e - tw_offset(s)) % q;
     double sn, cs;
-    sincospi((fa.inverse ? 2.0 : -2.0) * j / S, &sn, &cs);
-    tw[j] = C{(Rl)cs, (Rl)sn};
+    sincospi((fa.inverse ? 2.0 : -2.0) * (4 * lp + j) / (1 << s), &sn, &cs);
+    tw[e] = C{(Rl)cs, (Rl)sn};
   }
   uint4 r[T::IPT][T::V];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto load = [&](uint64_t tt) {
+    const uint64_t bi = tt >> a.m, y = tt & mmask;
+    const char* base = a.src + bi * a.src_bstride + (y << QZ) * E;
+#pragma unroll
+    for (int it = 0; it < T::IPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int c = id % T::CZ, g = id / T::CZ;
+#pragma unroll
+      for (int k = 0; k < T::V; ++k)
+        r[it][k] = ld_stream(base + (uint64_t)(g + k * T::GX) * src_row + (uint64_t)c * 16);
+    }
+  };
+  auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
 
   uint64_t t = blockIdx.x;
   if (t >= a.ntiles) return;
-  tile_load<E, Q, true>(r, a.src + (t >> a.m) * a.src_bstride + ((t & mmask) << Q) * E, row_stride);
+  load(t);
   for (;;) {
     const uint64_t bi = t >> a.m, y = t & mmask;
-    tile_stage<E, Q>(r, smem);
+#pragma unroll
+    for (int it = 0; it < T::IPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int c = id % T::CZ, g = id / T::CZ;
+      const int col = (int)(__brev((unsigned)g) >> (32 - (QX - T::LV)));
+      smem[sidx(c * T::V, col)] = xpose<E, 0>(r[it]);
+      if constexpr (T::V > 1) smem[sidx(c * T::V + 1, col)] = xpose<E, 1>(r[it]);
+    }
     __syncthreads();
     const uint64_t tn = t + gridDim.x;
-    if (tn < a.ntiles)
-      tile_load<E, Q, true>(r, a.src + (tn >> a.m) * a.src_bstride + ((tn & mmask) << Q) * E,
-                            row_stride);
-    char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << Q) * E;
-    if constexpr (Q == 6) {
-      fft_drain_q6<E, NWARPS>(smem, dbase, row_stride, tw, fa.stages, warp, lane, fa.inverse);
-    } else
-    // Q = 5: warp per destination row z, elements x' = lane in registers
-    for (int z = warp; z < S; z += NWARPS) {
-      C v[PER_LANE];
-#pragma unroll
-      for (int k = 0; k < PER_LANE; ++k) {
-        const int xp = lane + 32 * k;
-        const char* chunk = reinterpret_cast<const char*>(&smem[swz<E, Q>(z, xp / T::V)]);
-        v[k] = *reinterpret_cast<const C*>(chunk + (xp % T::V) * E);
-      }
-      const int s_lane = fa.stages < 5 ? fa.stages : 5;
-      for (int s = 1; s <= s_lane; ++s) {
-        const int half = 1 << (s - 1);
-        const C w = tw[(lane & (half - 1)) << (Q - s)];
-        const bool bottom = lane & half;
-#pragma unroll
-        for (int k = 0; k < PER_LANE; ++k) {
-          const C p = shfl_xor_c(v[k], half);
-          v[k] = bottom ? csub(p, cmul(v[k], w)) : cadd(v[k], cmul(p, w));
-        }
-      }
-      if constexpr (PER_LANE == 2) {
-        if (fa.stages >= 6) {  // x' and x' + 32 live in the same lane
-          const C t1 = cmul(v[1], tw[lane]);
-          v[1] = csub(v[0], t1);
-          v[0] = cadd(v[0], t1);
-        }
-      }
-      char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - Q)) * row_stride;
-#pragma unroll
-      for (int k = 0; k < PER_LANE; ++k)
-        *reinterpret_cast<C*>(drow + (uint64_t)(lane + 32 * k) * E) = v[k];
-    }
+    if (tn < a.ntiles) load(tn);
+    char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
+    fft_rows_drain<E, QX, QZ>(smem, dbase, dst_row, tw, fa.stages, fa.inverse != 0);
     if (tn >= a.ntiles) break;
     __syncthreads();
     t = tn;

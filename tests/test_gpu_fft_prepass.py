@@ -41,12 +41,12 @@ def rand_complex(shape, dtype, seed):
 
 
 @pytest.mark.parametrize("dtype", [torch.complex64, torch.complex128])
-@pytest.mark.parametrize("b,stages", [(10, 5), (12, 6), (14, 6), (16, 0), (16, 3), (20, 6),
-                                      (21, 5), (22, 6)])
+@pytest.mark.parametrize("b,stages", [(10, 5), (12, 6), (13, 7), (14, 6), (16, 0), (16, 3),
+                                      (17, 7), (20, 6), (21, 5), (22, 7)])
 @pytest.mark.parametrize("inverse", [False, True])
 def test_fused_stages_match_reference(cuda, dtype, b, stages, inverse):
-    if (1 << b) * (8 if dtype == torch.complex64 else 16) <= 32768 and b > 12:
-        pytest.skip("small-row path covered below")
+    if dtype == torch.complex128 and stages > 6 and (1 << b) * 16 > 32768:
+        pytest.skip("complex128 tiles fuse at most 6 stages")
     x = rand_complex(1 << b, dtype, b * 10 + stages)
     got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages, inverse=inverse)
     check(got, dit_reference(x, b, stages, inverse), dtype, stages)
@@ -78,12 +78,13 @@ def test_batched_and_host_arrays(cuda):
     check(got, dit_reference(x, b, stages), torch.complex128, stages)
 
 
-def test_completes_to_torch_fft(cuda):
-    """prepass (6 fused stages) + the remaining DIT stages in torch == torch.fft.fft."""
+@pytest.mark.parametrize("dtype,fused", [(torch.complex128, 6), (torch.complex64, 7)])
+def test_completes_to_torch_fft(cuda, dtype, fused):
+    """prepass (fused stages) + the remaining DIT stages in torch == torch.fft.fft."""
     b = 16
-    x = torch.from_numpy(rand_complex(1 << b, torch.complex128, 3)).to(cuda)
-    y = br.bitrev_dit_prepass(x, b, 6)
-    for s in range(7, b + 1):
+    x = torch.from_numpy(rand_complex(1 << b, dtype, 3)).to(cuda).to(torch.complex128)
+    y = br.bitrev_dit_prepass(x.to(dtype), b, fused).to(torch.complex128)
+    for s in range(fused + 1, b + 1):
         half = 1 << (s - 1)
         w = torch.exp(-2j * torch.pi * torch.arange(half, device=cuda, dtype=torch.float64)
                       / (2 * half))
@@ -91,7 +92,8 @@ def test_completes_to_torch_fft(cuda):
         u, v = blk[:, :half], blk[:, half:] * w
         y = torch.cat([u + v, u - v], dim=1).reshape(-1)
     ref = torch.fft.fft(x)
-    assert (y - ref).abs().max().item() <= 1e-9 * ref.abs().max().item()
+    tol = 1e-9 if dtype == torch.complex128 else 1e-5
+    assert (y - ref).abs().max().item() <= tol * ref.abs().max().item()
 
 
 def test_validation(cuda):
@@ -102,4 +104,6 @@ def test_validation(cuda):
     with pytest.raises(ValueError, match="stages"):
         br.bitrev_dit_prepass(z, 14, 15)
     with pytest.raises(br.BitrevError):
-        br.bitrev_dit_prepass(z, 14, 9)  # fused tiles carry at most 6 stages
+        br.bitrev_dit_prepass(z, 14, 9)  # complex64 tiles fuse at most 7 stages
+    assert br.max_fused_stages(14, 8) == 7 and br.max_fused_stages(14, 16) == 6
+    assert br.max_fused_stages(11, 16) == 11
