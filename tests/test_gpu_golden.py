@@ -164,3 +164,38 @@ def test_sharded_plan_kernels(cuda, b, G, dtype, chunks):
     outs = sharded.emulate_sharded(x, b, G, chunks)
     got = torch.cat(outs)
     assert torch.equal(got.view(torch.uint8), br.oracle_permute(x, b).view(torch.uint8))
+
+
+def _chunked_rev_check(out, b, chunk_bits=27):
+    """out[i] == rev_b(i) for every i, verified 2^chunk_bits indices at a time
+    with an independent torch shift loop (keeps the check's memory bounded)."""
+    dev = out.device
+    n = 1 << b
+    for start in range(0, n, 1 << chunk_bits):
+        idx = torch.arange(start, min(n, start + (1 << chunk_bits)), dtype=torch.int64, device=dev)
+        r = torch.zeros_like(idx)
+        v = idx.clone()
+        for _ in range(b):
+            r = (r << 1) | (v & 1)
+            v >>= 1
+        assert torch.equal(out[start:start + idx.numel()].to(torch.int64), r), start
+
+
+@pytest.mark.parametrize("b,inplace", [(31, True), (31, False), (32, True)])
+def test_sentinel_64bit_sizes(cuda, b, inplace):
+    """2^31 / 2^32 int64 elements (16 / 32 GiB): the sizes of BASELINE config
+    5's shards and beyond; exercises 64-bit offsets in every index path."""
+    free, _ = torch.cuda.mem_get_info(cuda)
+    need = (1 << b) * 8 * (1 if inplace else 2) + (6 << 30)
+    if free < need:
+        pytest.skip(f"needs {need >> 30} GiB free")
+    a = torch.arange(1 << b, dtype=torch.int64, device=cuda)
+    if inplace:
+        br.cobra_in_place(a, br.CobraConfig(6), b)
+        out = a
+    else:
+        out = torch.empty_like(a)
+        br.cobra_out_of_place(a, out, br.CobraConfig(6), b)
+        del a
+    torch.cuda.synchronize()
+    _chunked_rev_check(out, b)
