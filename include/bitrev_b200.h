@@ -175,8 +175,10 @@ int bitrev_set_tile_bits(int elem_bytes, int inplace, int q);
  * Staging path of the shared-memory kernels for (element size, family):
  * 0 = register staging (LDG.128 -> registers -> STS), 1 = TMA bulk ring
  * (cp.async.bulk row copies into a multi-stage shared-memory ring completing
- * on mbarriers).  Output never depends on it; a (q, path) pair that is not
- * instantiated falls back to path 0.  Initial value from the environment
+ * on mbarriers), 2 = TMA tensor ring (one cp.async.bulk.tensor per tile),
+ * 3 = rectangular register tiles (out of place only), 4 = element-granular
+ * cp.async into the transposed layout (in place only).  Output never depends
+ * on it; a (q, path) pair that is not instantiated falls back to path 0.  Initial value from the environment
  * (BITREV_B200_PATH_OOP / BITREV_B200_PATH_IP), else the measured default.
  */
 int bitrev_get_tile_path(int elem_bytes, int inplace);

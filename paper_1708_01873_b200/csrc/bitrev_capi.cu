@@ -235,6 +235,42 @@ int launch_ip_tile(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st)
 }
 
 // ---------------------------------------------------------------------------
+// in-place cp.async path (4): compact pairs only
+
+template <int E, int Q>
+int launch_ip_cpa(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  using T = CpaTile<E, Q>;
+  if (T::SMEM > 227 * 1024) return BITREV_ETILE;
+  auto kern = bitrev_inplace_cpa_kernel<E, Q>;
+  static int per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    return occupancy(kern, T::THREADS, T::SMEM);
+  }();
+  TileArgs a;
+  memset(&a, 0, sizeof a);
+  a.src = static_cast<const char*>(buf);
+  a.dst = static_cast<char*>(buf);
+  a.b = b;
+  a.m = b - 2 * Q;
+  a.src_bstride = bs * E;
+  a.dst_bstride = bs * E;
+  a.order = 2;
+  const int grid = set_pair_work(a, batch, true, per_sm);
+  kern<<<grid, T::THREADS, T::SMEM, st>>>(a);
+  return finish_launch();
+}
+
+int dispatch_ip_cpa(int E, int q, void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  if (E == 4 && q == 6) return launch_ip_cpa<4, 6>(buf, b, batch, bs, st);
+  if (E == 4 && q == 7) return launch_ip_cpa<4, 7>(buf, b, batch, bs, st);
+  if (E == 8 && q == 5) return launch_ip_cpa<8, 5>(buf, b, batch, bs, st);
+  if (E == 8 && q == 6) return launch_ip_cpa<8, 6>(buf, b, batch, bs, st);
+  if (E == 16 && q == 5) return launch_ip_cpa<16, 5>(buf, b, batch, bs, st);
+  if (E == 16 && q == 6) return launch_ip_cpa<16, 6>(buf, b, batch, bs, st);
+  return BITREV_ETILE;
+}
+
+// ---------------------------------------------------------------------------
 // TMA ring paths (1 = per-row bulk copies, 2 = tensor-map tiles)
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -623,6 +659,10 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
   if (vec_ok && (E == 4 || E == 8 || E == 16)) {
     const int path = tile_path(E, true);
     for (int q = pick_q(E, b, true, batch); q >= 3; --q) {
+      if (path == 4) {
+        rc = dispatch_ip_cpa(E, q, a, b, batch, batch_stride, st);
+        if (rc != BITREV_ETILE) return rc;
+      }
       if (path == 1 || path == 2) {
         rc = dispatch_ring(path, E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
         if (rc != BITREV_ETILE) return rc;
@@ -970,7 +1010,8 @@ int bitrev_get_tile_path(int elem_bytes, int inplace) { return tile_path(elem_by
 
 int bitrev_set_tile_path(int elem_bytes, int inplace, int path) {
   if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16) return BITREV_ETILE;
-  if (path < 0 || path > 3 || (path == 3 && inplace)) return BITREV_ETILE;
+  if (path < 0 || path > 4 || (path == 3 && inplace) || (path == 4 && !inplace))
+    return BITREV_ETILE;
   (inplace ? g_path_ip : g_path_oop)[elem_bytes].store(path);
   return BITREV_OK;
 }

@@ -43,6 +43,9 @@
 #ifndef BITREV_TILE_THREADS
 #define BITREV_TILE_THREADS 256  // threads per CTA of the register tile kernels
 #endif
+#ifndef BITREV_CPA_STAGES
+#define BITREV_CPA_STAGES 3  // pair stages of the cp.async in-place kernel
+#endif
 #ifndef BITREV_RING_BUDGET_KB
 #define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
 #endif
@@ -777,6 +780,124 @@ __global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
       c_next(c);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// in-place tile pairs through cp.async (LDGSTS) straight into the transposed
+// layout
+//
+// Every element is copied global -> shared by its own E-byte cp.async into
+// its destination slot U[z][rev_Q(x)] (the register kernel's staged layout),
+// so no registers hold in-flight data and no register transpose is needed.
+// NS pair stages rotate: while stage i is drained (LDS.128 -> STG.128), the
+// copies of pairs i+1 .. i+NS-1 are in flight (cp.async.wait_group).  Shared
+// layout per tile: rows z of 2^Q/V 16-byte chunks, chunk' = chunk ^ (z & 15)
+// (16 lanes writing one element each into 16 consecutive rows hit 16
+// distinct chunks; the drain reads whole rows, any per-row XOR is free).
+
+__device__ __forceinline__ void cp_async_e(uint32_t dst, const void* src, int bytes) {
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int E, int Q>
+struct CpaTile {
+  static constexpr int S = 1 << Q;
+  static constexpr int V = 16 / E;
+  static constexpr int CH = S / V;            // 16-byte chunks per smem row
+  static constexpr int TILE = S * S * E;
+  static constexpr int THREADS = 256;
+  static constexpr int EPT = S * S / THREADS;  // elements copied per thread per tile
+  static constexpr int WPT = S * CH / THREADS; // chunks drained per thread per tile
+  static constexpr int STAGES = BITREV_CPA_STAGES;
+  static constexpr int SMEM = STAGES * 2 * TILE;
+  static_assert(CH >= 16, "swizzle needs 16 chunks per row");
+};
+
+template <int E, int Q>
+__device__ __forceinline__ uint32_t cpa_slot(uint32_t tile, int z, int xp) {
+  using T = CpaTile<E, Q>;
+  const int col = xp / T::V, slot = xp % T::V;
+  return tile + (uint32_t)((z * T::CH + (col ^ (z & 15))) * 16 + slot * E);
+}
+
+template <int E, int Q>
+__device__ __forceinline__ void cpa_issue_tile(uint32_t tile, const char* src_tile,
+                                               uint64_t row_stride) {
+  using T = CpaTile<E, Q>;
+#pragma unroll
+  for (int it = 0; it < T::EPT; ++it) {
+    const int id = it * T::THREADS + threadIdx.x;
+    const int z = id % T::S, x = id / T::S;  // consecutive lanes: consecutive z of row x
+    const int xp = (int)(__brev((unsigned)x) >> (32 - Q));
+    cp_async_e(cpa_slot<E, Q>(tile, z, xp), src_tile + (uint64_t)x * row_stride + (uint64_t)z * E,
+               E);
+  }
+}
+
+template <int E, int Q>
+__device__ __forceinline__ void cpa_drain_tile(uint32_t tile, char* dst_base, uint64_t row_stride) {
+  using T = CpaTile<E, Q>;
+#pragma unroll
+  for (int it = 0; it < T::WPT; ++it) {
+    const int id = it * T::THREADS + threadIdx.x;
+    const int col = id % T::CH, z = id / T::CH;
+    const uint4 v = lds128(tile + (uint32_t)((z * T::CH + (col ^ (z & 15))) * 16));
+    const uint64_t rz = __brev((unsigned)z) >> (32 - Q);
+    st_vec(dst_base + rz * row_stride + (uint64_t)col * 16, v);
+  }
+}
+
+template <int E, int Q>
+__global__ void __launch_bounds__(CpaTile<E, Q>::THREADS)
+    bitrev_inplace_cpa_kernel(TileArgs a) {
+  using T = CpaTile<E, Q>;
+  extern __shared__ __align__(16) unsigned char smem_cpa[];
+  const uint32_t base = smem_u32(smem_cpa);
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  PairCursor issue_c, drain_c;
+  issue_c.start(a);
+  drain_c = issue_c;
+  auto issue = [&](int stage) {
+    if (issue_c.valid(a)) {
+      const uint64_t bi = issue_c.bi, y = pair_from_index(issue_c.w, a.m);
+      const uint64_t ry = dev_rev(y, a.m);
+      const char* src = a.src + bi * a.src_bstride;
+      const uint32_t st = base + stage * 2 * T::TILE;
+      cpa_issue_tile<E, Q>(st, src + (y << Q) * E, row_stride);
+      if (ry != y) cpa_issue_tile<E, Q>(st + T::TILE, src + (ry << Q) * E, row_stride);
+      issue_c.next(a);
+    }
+    cp_async_commit();  // one group per stage slot, possibly empty
+  };
+#pragma unroll
+  for (int s = 0; s < T::STAGES - 1; ++s) issue(s);
+  for (int i = 0; drain_c.valid(a); ++i) {
+    issue((i + T::STAGES - 1) % T::STAGES);  // slot drained at iteration i-1
+    cp_async_wait<T::STAGES - 1>();           // this thread's copies for stage i landed
+    __syncthreads();                          // ... and everyone else's
+    const int stage = i % T::STAGES;
+    const uint64_t bi = drain_c.bi, y = pair_from_index(drain_c.w, a.m);
+    const uint64_t ry = dev_rev(y, a.m);
+    const uint32_t st = base + stage * 2 * T::TILE;
+    char* dst = a.dst + bi * a.dst_bstride;
+    cpa_drain_tile<E, Q>(st, dst + (ry << Q) * E, row_stride);
+    if (ry != y) cpa_drain_tile<E, Q>(st + T::TILE, dst + (y << Q) * E, row_stride);
+    drain_c.next(a);
+    __syncthreads();  // stage i is refilled at iteration i+1
+  }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------

@@ -4,7 +4,8 @@ The reference tunes COBRA's block width q per size by timing candidates and
 keeping the fastest mean (ties toward the smaller buffer).  Here the knobs are
 the shared-memory tile bits Q and the staging path (0 = register staging,
 1 = per-row cp.async.bulk ring, 2 = TMA tensor-map ring, 3 = rectangular
-register tiles, out of place only) of each kernel family;
+register tiles, out of place only, 4 = element-granular cp.async pipeline, in
+place only) of each kernel family;
 the output never depends on them.  Candidates are timed in interleaved rounds
 (every candidate once per round) with CUDA events, so clock or box drift during
 the run hits all candidates alike.  Records use the reference CSV schema
