@@ -224,3 +224,39 @@ def test_launch_counter_moves(cuda):
     br.cobra_in_place(a, br.CobraConfig(6), 20)
     torch.cuda.synchronize()
     assert br.launch_count() == before + 1
+
+
+@pytest.mark.parametrize("E", [4, 8, 16, 2])
+@pytest.mark.parametrize("path", [0, 1, 2, 3, 4])
+def test_guard_bands_untouched(cuda, E, path):
+    """Out-of-bounds writes check (compute-sanitizer is closed on this pool):
+    every staging path runs on a batched slice that sits inside a buffer with
+    random guard bands before, between (row padding) and after the rows; the
+    bands must come out bit-identical and the rows correct."""
+    b, batch, pad = 14, 3, 4096
+    n = 1 << b
+    stride = n + pad  # row padding acts as an inner guard band
+    buf = torch.from_numpy(rand_bits(pad + batch * stride + pad, E, seed=900 + E + 10 * path)).to(cuda)
+    before = buf.clone()
+    rows = buf[pad:pad + batch * stride].view(batch, stride)[:, :n]
+    expected = torch.stack([br.oracle_permute(r.contiguous(), b) for r in rows])
+    inplace = path != 3
+    old = (br.get_tile_path(E, inplace), br.get_tile_path(E, False))
+    try:
+        if E in (4, 8, 16):
+            br.set_tile_path(E, inplace, path if path != 4 or inplace else 0)
+        if inplace:
+            br.bitrev_batched_inplace(rows, b)
+            got = rows
+        else:
+            out = torch.zeros(batch, n, dtype=buf.dtype, device=cuda)
+            got = br.bitrev_batched(rows, b, out)
+        torch.cuda.synchronize()
+    finally:
+        if E in (4, 8, 16):
+            br.set_tile_path(E, inplace, old[0])
+    assert_same(got, expected)
+    mask = torch.ones(buf.numel(), dtype=torch.bool, device=cuda)
+    if inplace:
+        mask[pad:pad + batch * stride].view(batch, stride)[:, :n] = False
+    assert torch.equal(buf.view(torch.uint8).view(-1, E)[mask], before.view(torch.uint8).view(-1, E)[mask])
