@@ -949,10 +949,10 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   if (!vec_ok) return BITREV_EALIGN;
   a.m = b - qx - qz;
   a.ntiles = (uint64_t)batch << a.m;
-#define FFT_LAUNCH(E_, QX_, QZ_)                                                             \
-  {                                                                                          \
+#define FFT_LAUNCH(E_, QX_, QZ_, S_)                                                       \
+  case S_: {                                                                                 \
     using T = Rect<E_, QX_, QZ_>;                                                            \
-    auto kern = bitrev_fft_rect_kernel<E_, QX_, QZ_>;                                        \
+    auto kern = bitrev_fft_rect_kernel<E_, QX_, QZ_, S_>;                                    \
     static int per_sm = [&] {                                                                \
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES);     \
       return occupancy(kern, T::THREADS, T::BYTES);                                          \
@@ -960,8 +960,19 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                      \
     return finish_launch();                                                                  \
   }
-  if (E == 8) FFT_LAUNCH(8, 7, 4)
-  if (E == 16) FFT_LAUNCH(16, 6, 3)
+  if (E == 8) {
+    switch (stages) {
+      FFT_LAUNCH(8, 7, 4, 0) FFT_LAUNCH(8, 7, 4, 1) FFT_LAUNCH(8, 7, 4, 2)
+      FFT_LAUNCH(8, 7, 4, 3) FFT_LAUNCH(8, 7, 4, 4) FFT_LAUNCH(8, 7, 4, 5)
+      FFT_LAUNCH(8, 7, 4, 6) FFT_LAUNCH(8, 7, 4, 7)
+    }
+  } else {
+    switch (stages) {
+      FFT_LAUNCH(16, 6, 3, 0) FFT_LAUNCH(16, 6, 3, 1) FFT_LAUNCH(16, 6, 3, 2)
+      FFT_LAUNCH(16, 6, 3, 3) FFT_LAUNCH(16, 6, 3, 4) FFT_LAUNCH(16, 6, 3, 5)
+      FFT_LAUNCH(16, 6, 3, 6)
+    }
+  }
 #undef FFT_LAUNCH
   return BITREV_ETILE;
 }

@@ -26,6 +26,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -45,6 +46,12 @@
 #endif
 #ifndef BITREV_CPA_STAGES
 #define BITREV_CPA_STAGES 3  // pair stages of the cp.async in-place kernel
+#endif
+#ifndef BITREV_FFT_MINB
+#define BITREV_FFT_MINB 1  // min CTAs/SM for the 5..7-stage FFT kernels (register cap)
+#endif
+#ifndef BITREV_FFT_RADIX4
+#define BITREV_FFT_RADIX4 1  // FFT pre-pass drain: radix-4 layout passes (1) or shuffles (0)
 #endif
 #ifndef BITREV_RING_BUDGET_KB
 #define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
@@ -1061,15 +1068,178 @@ __device__ __forceinline__ void fft_rows_drain(const uint4* U, char* dbase, uint
   }
 }
 
+// Radix-4 drain: the row's elements move between lane layouts through the
+// warp's own rows of the tile buffer (nobody else reads them after the load),
+// so every pair of stages is an in-register radix-4 pass:
+//   layout A: lane ll holds x' = 4 ll + m            stages 1, 2
+//   layout B: x' = (ll & 3) + 4 m + 16 (ll >> 2)      stages 3, 4
+//   layout C: x' = (ll & 15) + 16 m + 64 (ll >> 4)    stages 5, 6 (complex128:
+//             x' = ll + 16 m, natural for the store)
+//   layout D: x' = ll + 32 m  (complex64)             stage 7, natural store
+// Word x' of a row lives at swizzled position f(x'), chosen so that every
+// layout's 8-byte (complex64: x ^ 5 * ((x >> 4) & 3)) or 16-byte (complex128:
+// x ^ ((x >> 3) & 3) ^ (((x >> 4) & 1) << 2)) accesses are bank-conflict free.
+// Twiddles are lane constants kept in registers.
+template <int E>
+__device__ __forceinline__ int fft_swz(int x) {
+  if constexpr (E == 8) return x ^ (((x >> 4) & 3) * 5);
+  else return x ^ ((x >> 3) & 3) ^ (((x >> 4) & 1) << 2);
+}
+
+template <int E, int QX>
+__device__ __forceinline__ int fft_layout(int L, int ll, int m) {
+  switch (L) {
+    case 0: return 4 * ll + m;
+    case 1: return (ll & 3) + 4 * m + 16 * (ll >> 2);
+    case 2: return (E == 8) ? (ll & 15) + 16 * m + 64 * (ll >> 4) : ll + 16 * m;
+    default: return ll + 32 * m;
+  }
+}
+
+template <typename C>
+__device__ __forceinline__ void bfly(C& top, C& bot, C w) {
+  const C t = cmul(bot, w);
+  bot = csub(top, t);
+  top = cadd(top, t);
+}
+
+template <int E, int QX, int QZ, int stages>
+__device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_t dst_row,
+                                                  const typename Cplx<E>::T* tw, bool inverse) {
+  using C = typename Cplx<E>::T;
+  using T = Rect<E, QX, QZ>;
+  constexpr int V = T::V, LPR = (1 << QX) / 4, RPP = 32 / LPR;
+  constexpr int NWARPS = T::THREADS / 32;
+  constexpr int ROWS = 1 << QZ;
+  constexpr int NR = (ROWS + NWARPS * RPP - 1) / (NWARPS * RPP);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp * RPP >= ROWS) return;
+  const int h = lane / LPR, ll = lane % LPR;
+  auto row_of = [&](int i) { return (warp + i * NWARPS) * RPP + h; };
+  auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
+  // twiddles: W_{2^s}^k = tw[k << (QX - s)] (tw = W_{2^QX}^j, j < 2^(QX-1))
+  auto W = [&](int s, int k) { return tw[k << (QX - s)]; };
+  const C w4 = inverse ? C{0, 1} : C{0, -1};
+  const int a = ll & 3, b = ll & 15;
+  C v[NR][4];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {  // layout A straight from the staged tile
+    const int z = row_of(i);
+#pragma unroll
+    for (int c = 0; c < 4 / V; ++c) {
+      const uint4 q = U[sidx(z, (4 * ll) / V + c)];
+      if constexpr (E == 8) {
+        v[i][2 * c] = make_float2(__uint_as_float(q.x), __uint_as_float(q.y));
+        v[i][2 * c + 1] = make_float2(__uint_as_float(q.z), __uint_as_float(q.w));
+      } else {
+        v[i][c] = make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
+      }
+    }
+  }
+  __syncwarp();
+  int L = 0;  // compile-time after unrolling: stages is a template parameter
+  auto to_layout = [&](int Lnew) {  // through the warp's own rows of U
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      C* row = reinterpret_cast<C*>(U) + (size_t)row_of(i) * (1 << QX);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) row[fft_swz<E>(fft_layout<E, QX>(L, ll, m))] = v[i][m];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const C* row = reinterpret_cast<const C*>(U) + (size_t)row_of(i) * (1 << QX);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) v[i][m] = row[fft_swz<E>(fft_layout<E, QX>(Lnew, ll, m))];
+    }
+    __syncwarp();
+    L = Lnew;
+  };
+  const C one = C{1, 0};
+  // stages 1, 2 (layout A)
+  if constexpr (stages >= 1)
+#pragma unroll
+    for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][1], one); bfly(v[i][2], v[i][3], one); }
+  if constexpr (stages >= 2)
+#pragma unroll
+    for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][2], one); bfly(v[i][1], v[i][3], w4); }
+  // stages 3, 4 (layout B)
+  if constexpr (stages >= 3) {
+    to_layout(1);
+    const C w3 = W(3, a);
+#pragma unroll
+    for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][1], w3); bfly(v[i][2], v[i][3], w3); }
+    if constexpr (stages >= 4) {
+      const C w40 = W(4, a), w41 = W(4, a + 4);
+#pragma unroll
+      for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][2], w40); bfly(v[i][1], v[i][3], w41); }
+    }
+  }
+  // stages 5, 6 (layout C)
+  if constexpr (stages >= 5) {
+    to_layout(2);
+    const C w5 = W(5, b);
+#pragma unroll
+    for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][1], w5); bfly(v[i][2], v[i][3], w5); }
+    if constexpr (stages >= 6) {
+      const C w60 = W(6, b), w61 = W(6, b + 16);
+#pragma unroll
+      for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][2], w60); bfly(v[i][1], v[i][3], w61); }
+    }
+  }
+  // stage 7 (layout D, complex64 only)
+  if constexpr (QX >= 7) {
+    if constexpr (stages >= 7) {
+      to_layout(3);
+      const C w70 = W(7, ll), w71 = W(7, ll + 32);
+#pragma unroll
+      for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][2], w70); bfly(v[i][1], v[i][3], w71); }
+    }
+  }
+  // store from whatever layout the last stage left: for each m every layout's
+  // lanes cover whole 32-byte sectors (A: 4 contiguous per lane; B: runs of 4;
+  // C: runs of 16; D: 32 contiguous), so no final transpose is needed
+  auto store = [&](auto layout_tag) {
+    constexpr int LS = decltype(layout_tag)::value;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int z = row_of(i);
+      char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - QZ)) * dst_row;
+      if constexpr (LS == 0) {  // 4 contiguous elements per lane
+        char* p = drow + (uint64_t)(4 * ll) * E;
+        if constexpr (E == 8) {
+          st_vec(p, make_uint4(__float_as_uint(v[i][0].x), __float_as_uint(v[i][0].y),
+                               __float_as_uint(v[i][1].x), __float_as_uint(v[i][1].y)));
+          st_vec(p + 16, make_uint4(__float_as_uint(v[i][2].x), __float_as_uint(v[i][2].y),
+                                    __float_as_uint(v[i][3].x), __float_as_uint(v[i][3].y)));
+        } else {
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            st_vec(p + 16 * m, make_uint4(__double2loint(v[i][m].x), __double2hiint(v[i][m].x),
+                                          __double2loint(v[i][m].y), __double2hiint(v[i][m].y)));
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          *reinterpret_cast<C*>(drow + (uint64_t)fft_layout<E, QX>(LS, ll, m) * E) = v[i][m];
+      }
+    }
+  };
+  constexpr int LF = stages <= 2 ? 0 : stages <= 4 ? 1 : stages <= 6 ? 2 : 3;  // final layout
+  store(std::integral_constant<int, LF>{});
+  (void)L;
+}
+
 // Rectangular-tile FFT pre-pass (bitrev_oop_rect_kernel's load/stage path).
-template <int E, int QX, int QZ>
-__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
+template <int E, int QX, int QZ, int STAGES>
+__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS, STAGES >= 5 ? BITREV_FFT_MINB : 1)
     bitrev_fft_rect_kernel(FftArgs fa) {
   using T = Rect<E, QX, QZ>;
   using C = typename Cplx<E>::T;
   using Rl = typename Cplx<E>::R;
   extern __shared__ __align__(16) uint4 smem[];
   __shared__ C tw[(1 << QX) - 4];
+  __shared__ C twq[1 << (QX - 1)];  // W_{2^QX}^j for the radix-4 drain
   const TileArgs& a = fa.t;
   const uint64_t src_row = (uint64_t)E << (a.b - QX);
   const uint64_t dst_row = (uint64_t)E << (a.b - QZ);
@@ -1081,6 +1251,11 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
     double sn, cs;
     sincospi((fa.inverse ? 2.0 : -2.0) * (4 * lp + j) / (1 << s), &sn, &cs);
     tw[e] = C{(Rl)cs, (Rl)sn};
+  }
+  for (int j = threadIdx.x; j < (1 << (QX - 1)); j += blockDim.x) {
+    double sn, cs;
+    sincospi((fa.inverse ? 2.0 : -2.0) * j / (1 << QX), &sn, &cs);
+    twq[j] = C{(Rl)cs, (Rl)sn};
   }
   uint4 r[T::IPT][T::V];
   auto load = [&](uint64_t tt) {
@@ -1114,7 +1289,11 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) load(tn);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
-    fft_rows_drain<E, QX, QZ>(smem, dbase, dst_row, tw, fa.stages, fa.inverse != 0);
+    if (BITREV_FFT_RADIX4) {  // twq was published by the staging barrier above
+      fft_rows_drain_r4<E, QX, QZ, STAGES>(smem, dbase, dst_row, twq, fa.inverse != 0);
+    } else {
+      fft_rows_drain<E, QX, QZ>(smem, dbase, dst_row, tw, fa.stages, fa.inverse != 0);
+    }
     if (tn >= a.ntiles) break;
     __syncthreads();
     t = tn;
