@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <map>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -169,14 +170,34 @@ int grid_for_pairs(uint64_t work, int per_sm) {
   return g;
 }
 
-// Resident CTAs per SM of a kernel at a dynamic smem size (cached per instance
-// by the caller through a function-local static).
+// Resident CTAs per SM of a kernel at a dynamic smem size.
 template <typename K>
 int occupancy(K kernel, int threads, size_t smem) {
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess)
     n = 1;
   return n > 0 ? n : 1;
+}
+
+// Per-device launch setup of one kernel instantiation: raises its dynamic
+// shared-memory limit on the current device (an attribute is per device, so
+// a process driving several GPUs needs it on each) and caches its occupancy.
+std::mutex g_prep_mu;
+std::map<std::pair<const void*, int>, int> g_prep;  // (kernel, device) -> CTAs per SM
+
+template <typename K>
+int prepare_kernel(K kernel, int threads, int smem_bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+  std::lock_guard<std::mutex> lk(g_prep_mu);
+  auto it = g_prep.find(key);
+  if (it != g_prep.end()) return it->second;
+  if (smem_bytes > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  const int v = occupancy(kernel, threads, smem_bytes);
+  g_prep.emplace(key, v);
+  return v;
 }
 
 // ---------------------------------------------------------------------------
@@ -187,10 +208,7 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
                     cudaStream_t st) {
   using T = Tile<E, Q>;
   auto kern = bitrev_oop_tile_kernel<E, Q>;
-  static int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES);
-    return occupancy(kern, T::THREADS, T::BYTES);
-  }();
+  const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
   TileArgs a;
   a.src = static_cast<const char*>(src);
   a.dst = static_cast<char*>(dst);
@@ -211,10 +229,7 @@ template <int E, int Q, bool COMPACT>
 int launch_ip_tile_mode(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
   using T = Tile<E, Q>;
   auto kern = bitrev_inplace_tile_kernel<E, Q, COMPACT>;
-  static int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * T::BYTES);
-    return occupancy(kern, T::THREADS, 2 * T::BYTES);
-  }();
+  const int per_sm = prepare_kernel(kern, T::THREADS, 2 * T::BYTES);
   TileArgs a;
   a.src = static_cast<const char*>(buf);
   a.dst = static_cast<char*>(buf);
@@ -242,10 +257,7 @@ int launch_ip_cpa(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) 
   using T = CpaTile<E, Q>;
   if (T::SMEM > 227 * 1024) return BITREV_ETILE;
   auto kern = bitrev_inplace_cpa_kernel<E, Q>;
-  static int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-    return occupancy(kern, T::THREADS, T::SMEM);
-  }();
+  const int per_sm = prepare_kernel(kern, T::THREADS, T::SMEM);
   TileArgs a;
   memset(&a, 0, sizeof a);
   a.src = static_cast<const char*>(buf);
@@ -318,10 +330,7 @@ int launch_ring_mode(const void* src, void* dst, int b, int64_t batch, int64_t s
   memset(&map, 0, sizeof map);
   if (MODE == kTensor && !encode_tile_map(&map, src, b, E, Q, batch, sbs)) return BITREV_ETILE;
   auto kern = bitrev_ring_kernel<E, Q, INPLACE, MODE, COMPACT>;
-  static int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, R::SMEM);
-    return occupancy(kern, R::THREADS, R::SMEM);
-  }();
+  const int per_sm = prepare_kernel(kern, R::THREADS, R::SMEM);
   TileArgs a;
   a.src = static_cast<const char*>(src);
   a.dst = static_cast<char*>(dst);
@@ -377,10 +386,7 @@ int launch_oop_rect(const void* src, void* dst, int b, int64_t batch, int64_t sb
   using T = Rect<E, QX, QZ>;
   if (b < QX + QZ) return BITREV_ETILE;
   auto kern = bitrev_oop_rect_kernel<E, QX, QZ>;
-  static int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES);
-    return occupancy(kern, T::THREADS, T::BYTES);
-  }();
+  const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
   TileArgs a;
   a.src = static_cast<const char*>(src);
   a.dst = static_cast<char*>(dst);
@@ -486,10 +492,7 @@ int launch_small(const void* src, void* dst, int b, int64_t batch, int64_t sbs, 
                  cudaStream_t st) {
   const int bytes = (1 << b) * E;
   auto kern = bitrev_small_kernel<E>;
-  static int per_sm = [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallBytes);
-    return occupancy(kern, 256, kSmallBytes);
-  }();
+  const int per_sm = prepare_kernel(kern, 256, kSmallBytes);
   const int threads = (1 << b) < 256 ? ((1 << b) < 32 ? 32 : (1 << b)) : 256;
   const int grid = grid_for((uint64_t)batch, per_sm * (256 / threads));
   kern<<<grid, threads, bytes, st>>>(static_cast<const char*>(src), static_cast<char*>(dst), b,
@@ -930,10 +933,10 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     const int bytes = (int)(n * E);
     const int grid = grid_for((uint64_t)batch, 8);
     if (E == 8) {
-      cudaFuncSetAttribute(fft_prepass_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallBytes);
+      prepare_kernel(fft_prepass_small_kernel<8>, 256, kSmallBytes);
       fft_prepass_small_kernel<8><<<grid, 256, bytes, st>>>(fa);
     } else {
-      cudaFuncSetAttribute(fft_prepass_small_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallBytes);
+      prepare_kernel(fft_prepass_small_kernel<16>, 256, kSmallBytes);
       fft_prepass_small_kernel<16><<<grid, 256, bytes, st>>>(fa);
     }
     return finish_launch();
@@ -953,10 +956,7 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   case S_: {                                                                                 \
     using T = Rect<E_, QX_, QZ_>;                                                            \
     auto kern = bitrev_fft_rect_kernel<E_, QX_, QZ_, S_>;                                    \
-    static int per_sm = [&] {                                                                \
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES);     \
-      return occupancy(kern, T::THREADS, T::BYTES);                                          \
-    }();                                                                                     \
+    const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);                           \
     kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                      \
     return finish_launch();                                                                  \
   }
