@@ -83,6 +83,8 @@ def parse():
                     help="override the staging path (0 reg, 1 bulk ring, 2 tensor ring, 3 rect)")
     ap.add_argument("--chunks", type=int, default=4,
                     help="cfg5: sub-chunks per all-to-all (exchange/unpack overlap)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="cfg5: fused scatter into peer-mapped symmetric memory instead of NCCL")
     ap.add_argument("--no-soak", action="store_true",
                     help="skip the 0.5 s clock soak (for profiler runs)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0,
@@ -350,7 +352,18 @@ def main():
         _lib.set_tile_bits(E, inplace, args.tile_bits)
     if args.tile_path >= 0:
         _lib.set_tile_path(E, inplace, args.tile_path)
-    if args.workload == "cfg5":
+    exchange = "nccl all_to_all"
+    if args.workload == "cfg5" and args.p2p:
+        try:
+            peers, p2p_barrier, _keep = sharded.symmetric_recv(n_local, dtype, dev)
+            exchange = "fused scatter into symmetric memory (NVLink peer stores)"
+
+            def step():
+                return sharded.sharded_bitrev_p2p(x, b, peers, rank, p2p_barrier)
+        except Exception as exc:  # no peer mapping available: report and use NCCL
+            exchange = f"nccl all_to_all (p2p unavailable: {type(exc).__name__})"
+            args.p2p = False
+    if args.workload == "cfg5" and not args.p2p:
         def step():
             return sharded.sharded_bitrev(x, b, chunks=args.chunks)
     elif args.workload == "cfg4-fft7":
@@ -560,7 +573,8 @@ def main():
                     "max": max(step_s) * 1e3},
     }
     if args.workload == "cfg5":
-        line["roofline"]["kernel"] = "local bitrev + NCCL all-to-all + unpack"
+        line["roofline"]["kernel"] = f"local bitrev + {exchange} + unpack"
+        line["config"]["exchange"] = exchange
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args.workload, args.cpu_sample_s)

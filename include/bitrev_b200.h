@@ -153,6 +153,20 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
                        int inverse, void* stream);
 
 /*
+ * Steps 1+2 of the top-bit sharded plan fused (no reference counterpart;
+ * SURVEY.md 8(e)): rank `rank` of G = 2^g bit-reverses its local shard of
+ * 2^b_local elements and stores each destination row straight into
+ * peer_recv[d] (the receive buffer of rank d, G entries, G <= 8) at element
+ * rank*C + k, C = 2^(b_local-g) -- i.e. what the all-to-all would deliver.
+ * With peer pointers mapped over NVLink/NVSwitch (symmetric memory or CUDA
+ * IPC) the stores cross the fabric from the SMs; after a cross-rank barrier
+ * every rank runs bitrev_sharded_unpack on its receive buffer.  Requires
+ * b_local - g >= the tile bits (rows never straddle two chunks).
+ */
+int bitrev_sharded_scatter(const void* local, void* const* peer_recv, int b_local, int g, int rank,
+                           int elem_bytes, void* stream);
+
+/*
  * Step 3 of the top-bit sharded plan (no reference counterpart: the reference
  * has no multi-device path).  recv holds G = 2^g
  * chunks of C = 2^(b_local-g) elements, chunk r received from rank r;

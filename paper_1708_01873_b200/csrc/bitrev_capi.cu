@@ -977,6 +977,44 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   return BITREV_ETILE;
 }
 
+int bitrev_sharded_scatter(const void* local, void* const* peer_recv, int b_local, int g, int rank,
+                           int elem_bytes, void* stream) {
+  const int E = elem_bytes;
+  if (b_local < 1 || b_local > kMaxBits) return BITREV_EWIDTH;
+  if (E != 4 && E != 8 && E != 16) return BITREV_EELEM;
+  if (g < 0 || (1 << g) > kMaxPeers || rank < 0 || rank >= (1 << g)) return BITREV_ESHARD;
+  if (!local || !peer_recv) return BITREV_ENULL;
+  const int q = E == 4 ? 6 : 5;  // 256 / 256 / 512-byte rows
+  if (b_local - g < q || 2 * q > b_local) return BITREV_ESHARD;  // rows inside one chunk
+  ScatterArgs sa;
+  memset(&sa, 0, sizeof sa);
+  for (int d = 0; d < (1 << g); ++d) {
+    if (!peer_recv[d] || !aligned16(peer_recv[d])) return BITREV_ENULL;
+    sa.peer[d] = static_cast<char*>(peer_recv[d]);
+  }
+  if (!aligned16(local)) return BITREV_EALIGN;
+  sa.g = g;
+  sa.rank = rank;
+  TileArgs& a = sa.t;
+  a.src = static_cast<const char*>(local);
+  a.b = b_local;
+  a.m = b_local - 2 * q;
+  a.ntiles = 1ull << a.m;
+  a.batch = 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define SCATTER(E_, Q_)                                                                   \
+  if (E == E_ && q == Q_) {                                                               \
+    using T = Tile<E_, Q_>;                                                               \
+    auto kern = bitrev_scatter_tile_kernel<E_, Q_>;                                       \
+    const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);                        \
+    kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(sa);                   \
+    return finish_launch();                                                               \
+  }
+  SCATTER(4, 6) SCATTER(8, 5) SCATTER(16, 5)
+#undef SCATTER
+  return BITREV_ETILE;
+}
+
 int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int elem_bytes,
                           void* stream) {
   const int E = elem_bytes;

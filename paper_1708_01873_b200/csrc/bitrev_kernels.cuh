@@ -451,6 +451,64 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
 }
 
 // ---------------------------------------------------------------------------
+// sharded plan, steps 1+2 fused: local bit reversal scattered to peers
+//
+// Rank `rank` of G = 2^g reverses its (b-g)-bit shard; the local output index
+// u = d*C + k (C = 2^(b-2g)) belongs to rank d = u >> (b-2g) at position
+// rank*C + k of that rank's receive buffer.  A tile's
+// destination row is 2^Q contiguous u inside one chunk d (C >= 2^Q), so the
+// drain just swaps its base pointer for peer[d] + (rank*C + k0)*E: with peer
+// pointers mapped over NVLink/NVSwitch (symmetric memory / CUDA IPC) the row
+// stores go straight into the peers' HBM -- no send buffer, no separate
+// all-to-all pass.  On one device the same kernel runs with G local buffers.
+
+constexpr int kMaxPeers = 8;
+
+struct ScatterArgs {
+  TileArgs t;
+  char* peer[kMaxPeers];  // receive buffer of each rank
+  int g;                  // log2 G
+  int rank;
+};
+
+template <int E, int Q>
+__global__ void __launch_bounds__(Tile<E, Q>::THREADS)
+    bitrev_scatter_tile_kernel(ScatterArgs sa) {
+  using T = Tile<E, Q>;
+  extern __shared__ __align__(16) uint4 smem[];
+  const TileArgs& a = sa.t;
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const uint64_t mmask = (1ull << a.m) - 1;
+  const int cbits = a.b - sa.g;  // log2 C, a.b = local width b - g
+  uint4 r[T::IPT][T::V];
+  uint64_t t = blockIdx.x;
+  if (t >= a.ntiles) return;
+  tile_load<E, Q, true>(r, a.src + ((t & mmask) << Q) * E, row_stride);
+  for (;;) {
+    const uint64_t y = t & mmask;
+    tile_stage<E, Q>(r, smem);
+    __syncthreads();
+    const uint64_t tn = t + gridDim.x;
+    if (tn < a.ntiles) tile_load<E, Q, true>(r, a.src + ((tn & mmask) << Q) * E, row_stride);
+    const uint64_t ry_base = dev_rev(y, a.m) << Q;
+#pragma unroll
+    for (int it = 0; it < T::WPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int col = id % T::CH;
+      const int z = id / T::CH;
+      const uint4 v = smem[swz<E, Q>(z, col)];
+      const uint64_t u0 = ((uint64_t)(__brev((unsigned)z) >> (32 - Q)) << (a.b - Q)) | ry_base;
+      const int d = (int)(u0 >> cbits);
+      const uint64_t k0 = u0 & ((1ull << cbits) - 1);
+      st_vec(sa.peer[d] + (((uint64_t)sa.rank << cbits) + k0) * E + (uint64_t)col * 16, v);
+    }
+    if (tn >= a.ntiles) break;
+    __syncthreads();
+    t = tn;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // in-place tile-pair kernel (replaces _cobra_swap, src/permutations.py:252-285)
 //
 // Work item y (per batch row) with y <= rev(y): load tile y and tile rev(y) into

@@ -12,12 +12,17 @@ and rev_{b-g}(j) = rev_g(l)*2^(b-2g) + rev_{b-2g}(m), so:
              rank d receives recv[r] = L_r[d];
   3. local:  out[k*G + rev_g(r)] = recv[r][k]    -- bitrev_sharded_unpack.
 
+sharded_bitrev_p2p fuses steps 1 and 2 for ranks that share peer-mapped
+memory (one NVLink/NVSwitch node): the tile kernel's destination rows are
+stored straight into the owning rank's receive buffer.
+
 Requires b >= 2g.  Each element crosses HBM twice per local step and NVLink
 once (unless it stays on its own rank: 1/G of the data).
 """
 
 from __future__ import annotations
 
+import ctypes
 from typing import Callable
 
 import torch
@@ -104,6 +109,74 @@ def sharded_bitrev(local: torch.Tensor, b: int, group=None, *, chunks: int = 1,
             works[c].wait()
         unpack(recv[c].reshape(-1), b_local - kb, g, out[c * sub * G:(c + 1) * sub * G])
     return out
+
+
+def _scatter(local: torch.Tensor, b_local: int, g: int, rank: int, peers: list) -> None:
+    """Steps 1+2 fused: local bitrev stored straight into the G receive buffers."""
+    ptrs = (ctypes.c_void_p * len(peers))(*[p.data_ptr() for p in peers])
+    with torch.cuda.device(local.device):
+        _lib.call("bitrev_sharded_scatter", local.data_ptr(), ctypes.cast(ptrs, ctypes.c_void_p),
+                  b_local, g, rank, _core.elem_bytes(local), _core._stream_ptr(local.device))
+
+
+def sharded_bitrev_p2p(local: torch.Tensor, b: int, peer_recv: list, rank: int,
+                       barrier: Callable) -> torch.Tensor:
+    """Peer-memory variant of sharded_bitrev for one NVLink/NVSwitch node.
+
+    peer_recv[d] is rank d's receive buffer (2^(b-g) elements) mapped into
+    this process -- e.g. the peer views of a torch symmetric-memory allocation
+    or CUDA IPC handles.  The local reversal writes its rows straight into the
+    peers' buffers (bitrev_sharded_scatter: no send buffer, no NCCL pass);
+    `barrier()` must order every rank's stores before any rank reads its
+    buffer (a device-side or stream-synchronised cross-rank barrier); then the
+    interleave runs locally.  Returns this rank's shard of the permuted array.
+    """
+    world = len(peer_recv)
+    g = check_plan(b, world)
+    b_local = b - g
+    if local.dim() != 1 or local.shape[0] != (1 << b_local):
+        raise ValueError(f"local shard length {local.shape[0]} does not match 2**{b_local}")
+    _scatter(local.contiguous(), b_local, g, rank, peer_recv)
+    barrier()
+    out = torch.empty_like(local)
+    _unpack(peer_recv[rank], b_local, g, out)
+    return out
+
+
+def symmetric_recv(n: int, dtype, device, group=None):
+    """Receive buffers for sharded_bitrev_p2p from torch symmetric memory.
+
+    Returns (peer_views, barrier, handle): peer_views[d] is rank d's
+    n-element buffer mapped into this process, barrier() is the handle's
+    stream-ordered cross-rank barrier (it publishes the peers' stores), and
+    the handle must be kept alive while the buffers are used.  Needs a node
+    whose GPUs can map each other's memory (NVLink/NVSwitch); not exercised
+    in the single-GPU test runs of this repo.
+    """
+    import torch.distributed._symmetric_memory as symm
+
+    buf = symm.empty(n, dtype=dtype, device=device)
+    hdl = symm.rendezvous(buf, group or dist.group.WORLD)
+    peers = [hdl.get_buffer(r, (n,), dtype) for r in range(hdl.world_size)]
+    return peers, (lambda: hdl.barrier()), (hdl, buf)
+
+
+def emulate_sharded_p2p(global_array: torch.Tensor, b: int, world_size: int) -> list[torch.Tensor]:
+    """All ranks of sharded_bitrev_p2p on ONE device: the peer table holds G
+    local receive buffers, so the fused scatter kernel and the unpack run
+    exactly as on a node (the stores just do not cross NVLink)."""
+    g = check_plan(b, world_size)
+    S = 1 << (b - g)
+    recv = [torch.empty(S, dtype=global_array.dtype, device=global_array.device)
+            for _ in range(world_size)]
+    for r in range(world_size):
+        _scatter(global_array[r * S:(r + 1) * S].contiguous(), b - g, g, r, recv)
+    outs = []
+    for d in range(world_size):
+        out = torch.empty_like(recv[d])
+        _unpack(recv[d], b - g, g, out)
+        outs.append(out)
+    return outs
 
 
 def emulate_sharded(global_array: torch.Tensor, b: int, world_size: int,
