@@ -28,12 +28,13 @@ std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_q_oop[17];
 std::atomic<int> g_q_ip[17];
 
-// Defaults from tools/tune_all.py on B200 (interleaved rounds, b = 26 and 30;
-// profiles/tune_r01*.jsonl): tile bits Q and staging path per (E, family).
+// Defaults from tools/tune_all.py / tools/oop_sizes.py on B200 (interleaved
+// rounds; profiles/tune_r01*.jsonl): tile bits Q and staging path per
+// (E, family).
 int default_q(int E, bool inplace) {
   switch (E) {
     case 4: return inplace ? 6 : 7;
-    case 8: return 6;
+    case 8: return inplace ? 6 : 7;   // out of place: rectangular QX = 7 (path 3)
     case 16: return inplace ? 5 : 6;
     default: return 0;
   }
@@ -72,7 +73,7 @@ std::atomic<int> g_path_ip[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1
 int default_path(int E, bool inplace) {
   if (inplace) return 0;  // register tile pairs (compact pair enumeration)
   switch (E) {
-    case 8: return 1;     // per-row cp.async.bulk ring
+    case 8: return 3;     // rectangular register tiles (1 KB destination rows)
     default: return 0;    // register tiles
   }
 }

@@ -39,9 +39,10 @@ class TileTuneResult:
 
 
 def tune_tiles(elem_bytes: int, inplace: bool, b: int, candidates=None, rounds: int = 5,
-               launches: int = 5, apply: bool = True, device=None) -> TileTuneResult:
-    """Time every (q, path) candidate on a random 2^b array; optionally make
-    the fastest the library's setting for (elem_bytes, family)."""
+               launches: int = 5, apply: bool = True, device=None,
+               batch: int = 1) -> TileTuneResult:
+    """Time every (q, path) candidate on `batch` random rows of 2^b elements;
+    optionally make the fastest the library's setting for (elem_bytes, family)."""
     if elem_bytes not in QS:
         raise ValueError("tile kernels exist for 4, 8 and 16-byte elements")
     cands = list(candidates) if candidates is not None else [
@@ -57,8 +58,10 @@ def tune_tiles(elem_bytes: int, inplace: bool, b: int, candidates=None, rounds: 
         raise ValueError(f"candidates {bad} are not valid tile bits for b={b}")
     dev = torch.device(device) if device is not None else _core.require_cuda()
     n = 1 << b
-    x = torch.empty(n * elem_bytes, dtype=torch.uint8, device=dev).random_(0, 256)
+    x = torch.empty(batch * n * elem_bytes, dtype=torch.uint8, device=dev).random_(0, 256)
     x = x.view(DTYPES[elem_bytes])
+    if batch > 1:
+        x = x.view(batch, n)
     y = None if inplace else torch.empty_like(x)
     old = (_lib.get_tile_bits(elem_bytes, inplace), _lib.get_tile_path(elem_bytes, inplace))
     samples: dict[tuple[int, int], list[float]] = {c: [] for c in cands}
@@ -85,13 +88,13 @@ def tune_tiles(elem_bytes: int, inplace: bool, b: int, candidates=None, rounds: 
                 e.synchronize()
                 dt = s.elapsed_time(e) / 1e3 / launches
                 samples[(q, p)].append(dt)
-                result.records.append(make_record(f"gpu_q{q}_p{p}", b, rnd, dt))
+                result.records.append(make_record(f"gpu_q{q}_p{p}", b, rnd, dt / batch))
     finally:
         _lib.set_tile_bits(elem_bytes, inplace, old[0])
         _lib.set_tile_path(elem_bytes, inplace, old[1])
     for c, ts in samples.items():
         ts = sorted(ts)
-        result.gbs[c] = 2 * n * elem_bytes / ts[len(ts) // 2] / 1e9
+        result.gbs[c] = 2 * batch * n * elem_bytes / ts[len(ts) // 2] / 1e9
     result.best = max(cands, key=lambda c: (result.gbs[c], -c[0]))
     if apply:
         _lib.set_tile_bits(elem_bytes, inplace, result.best[0])
