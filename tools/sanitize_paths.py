@@ -27,6 +27,8 @@ def same(a, b):
 
 
 checks = 0
+saved = {(E, ip): (br.get_tile_bits(E, ip), br.get_tile_path(E, ip))
+         for E in (4, 8, 16) for ip in (False, True)}
 for E in (4, 8, 16):
     for path in (0, 1, 2, 3, 4):
         for b in (13, 14):
@@ -45,8 +47,8 @@ for E in (4, 8, 16):
                         same(br.bitrev_batched(x, b), ref)
                     checks += 1
         for ip in (False, True):
-            br.set_tile_bits(E, ip, 0)
-            br.set_tile_path(E, ip, 0 if ip else {4: 0, 8: 1, 16: 0}[E])
+            br.set_tile_bits(E, ip, saved[(E, ip)][0])
+            br.set_tile_path(E, ip, saved[(E, ip)][1])
 for E in (1, 2, 4, 8, 16):  # small path, and element-wise fallbacks via misalignment
     x = rnd((1 << 10) + 1, E)
     v = x[1:]
