@@ -23,6 +23,19 @@
 //      (LDS.128) and writes it to destination row rev_Q(z) (STG.128).
 // The persistent loop issues the next tile's loads before draining the current
 // one, so every warp keeps V*IPT 16-byte loads in flight across the drain.
+//
+// Kernel families in this file (selection and measured defaults: bitrev_capi.cu)
+//   bitrev_oop_tile_kernel       out of place, square register tiles (above)
+//   bitrev_oop_rect_kernel       out of place, 2^QX x 2^QZ register tiles: short
+//                                source pieces, 1 KB destination rows
+//   bitrev_inplace_tile_kernel   in place, tile PAIRS {y, rev y}; work items from
+//                                the compact pair enumeration (pair_from_index)
+//   bitrev_ring_kernel           warp-specialised TMA ring: cp.async.bulk rows or
+//                                one cp.async.bulk.tensor per tile, mbarriers
+//   bitrev_inplace_cpa_kernel    in place through element-granular cp.async
+//   bitrev_scatter_tile_kernel   sharded plan: local reversal stored into peers
+//   bitrev_fft_rect_kernel       FFT pre-pass: rect tiles + up to 7 DIT stages
+//   small / gather / swap / transpose / even-odd / pairs / unpack kernels
 #pragma once
 
 #include <cstdint>
@@ -30,8 +43,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-// Build-time tuning knobs (defaults are the measured best; tools/variants.sh
-// builds alternatives side by side for A/B runs).
+// Build-time tuning knobs (defaults are the measured best).  Alternatives are
+// built side by side with `python -m paper_1708_01873_b200.build --out F -DKNOB=V`
+// and loaded through BITREV_B200_LIB for A/B runs (tools/*_ab.py).  The two
+// EXPERIMENT knobs produce WRONG output on purpose (timing-only builds).
 #ifndef BITREV_IP_NC
 #define BITREV_IP_NC 0  // in-place loads through the non-coherent path
 #endif
