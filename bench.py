@@ -278,6 +278,53 @@ def short_dtype(name):
     return {"float32": "f32", "float64": "f64", "complex64": "c64", "complex128": "c128"}[name]
 
 
+def host_info():
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        import psutil
+
+        info["physical_cores"] = psutil.cpu_count(logical=False)
+        info["ram_gb"] = round(psutil.virtual_memory().total / 2**30, 1)
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return info
+
+
+def single_thread_methods(workload, budget_s=20.0):
+    """The reference's single-thread methods on the same array:
+    COBRA (q = default_cobra_q), semi-recursive and recursive, once each, GB/s."""
+    from oracle import oracle as orc
+
+    b, dtname, E, inplace, batch, _ = WORKLOADS[workload]
+    if workload.startswith("cfg4") or workload == "cfg5" or (1 << b) * E > (2 << 30):
+        return None
+    np_dt = {"float32": np.float32, "float64": np.float64, "complex64": np.complex64,
+             "complex128": np.complex128}[dtname]
+    a = np.empty(1 << b, dtype=np_dt)
+    a.fill(1)  # touch every page before timing
+    q = min(b // 2, 6)
+    runs = [("cobra_in_place" if inplace else "cobra_out_of_place",
+             (lambda: orc.c_cobra_inplace(a, b, q)) if inplace else (lambda: orc.c_cobra_oop(a, b, q))),
+            ("semi_recursive_permute", lambda: orc.c_recursive(a, b, 9, 1)),
+            ("recursive_permute", lambda: orc.c_recursive(a, b, 9, 0))]
+    out = {}
+    t_all = time.perf_counter()
+    for name, fn in runs:
+        if time.perf_counter() - t_all > budget_s:
+            break
+        t0 = time.perf_counter()
+        fn()
+        out[name] = round(2 * a.nbytes / (time.perf_counter() - t0) / 1e9, 3)
+    return {"unit": "GB/s", "threads": 1, "values": out}
+
+
 def cpu_baseline(workload, target_s):
     """The C port timed on the host cores, bounded to ~target_s of CPU work."""
     threads = os.cpu_count() or 1
@@ -295,7 +342,8 @@ def cpu_baseline(workload, target_s):
     return {"value": nbytes * len(ts) / total / 1e9, "unit": "GB/s", "cores": threads,
             "kind": kind, "sample": f"{sample}, {len(ts)} steps",
             "method": "parallel_semi_recursive_permute (C port of src/parallel.py:95-156)"
-            if not workload.startswith("cfg4") else "cobra_in_place per row on a thread pool"}
+            if not workload.startswith("cfg4") else "cobra_in_place per row on a thread pool",
+            "host": host_info(), "single_thread": single_thread_methods(workload)}
 
 
 # ---------------------------------------------------------------------------
