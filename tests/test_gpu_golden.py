@@ -211,3 +211,22 @@ def test_sharded_p2p_scatter_kernel(cuda, b, G, dtype):
                     device=cuda).random_(0, 256).view(dtype)
     got = torch.cat(sharded.emulate_sharded_p2p(x, b, G))
     assert torch.equal(got.view(torch.uint8), br.oracle_permute(x, b).view(torch.uint8))
+
+
+@pytest.mark.parametrize("c", [c for c in GOLDEN["cases"] if c["b"] in (5, 12, 17) and
+                               c["recipe"] == "bits"], ids=case_id)
+def test_numpy_callers_get_reference_bytes(cuda, c):
+    """Drop-in: every method id driven with NUMPY arrays (the reference's own
+    array type) is staged through the device and matches the reference digest;
+    out-of-place results come back as numpy arrays."""
+    x = make_input(c["recipe"], c["E"], c["b"], c["trial"])
+    for m in br.METHOD_IDS:
+        a = x.copy()
+        out = br.make_method(m)(a, c["b"])
+        got = a if out is None else out
+        assert isinstance(got, np.ndarray), m
+        assert hashlib.sha256(np.ascontiguousarray(got).view(np.uint8).tobytes()).hexdigest() \
+            == c["output_sha256"], m
+    o = br.oracle_permute(x, c["b"])
+    assert isinstance(o, np.ndarray)
+    assert hashlib.sha256(o.view(np.uint8).tobytes()).hexdigest() == c["output_sha256"]
