@@ -478,6 +478,7 @@ def main():
     torch.cuda.synchronize()
     t_wall1 = time.monotonic()
     launches = _lib.launch_count() - launches0
+    chosen = _lib.last_tile()  # (tile bits, staging path) the timed launches used
     if world > 1:
         dist.barrier()
     step_s = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
@@ -570,6 +571,34 @@ def main():
                 e2e_single = rec
         if e2e is None:
             e2e = e2e_single
+        else:
+            # PCIe ceiling for the pipeline, same harness: each step one H2D and one
+            # D2H of the step's bytes on two streams, nothing else (no kernel).
+            d_in, d_out = torch.empty_like(x), torch.empty_like(x)
+            h_out = houts if houts is not None else hosts
+            s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
+            for timed in (False, True):
+                torch.cuda.synchronize()
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record(stream)
+                s_up.wait_stream(stream)
+                s_down.wait_stream(stream)
+                for k in range(reps if timed else 2):
+                    with torch.cuda.stream(s_up):
+                        d_in.copy_(hosts[k % nhost], non_blocking=True)
+                    with torch.cuda.stream(s_down):
+                        h_out[(k + 1) % nhost].copy_(d_out, non_blocking=True)
+                stream.wait_stream(s_up)
+                stream.wait_stream(s_down)
+                ev1.record(stream)
+                torch.cuda.synchronize()
+            ceil = bytes_local / (ev0.elapsed_time(ev1) / 1e3 / reps) / 1e9
+            e2e["pcie_ceiling_gbs"] = ceil
+            e2e["frac_of_pcie_ceiling"] = e2e["value"] / ceil
+            e2e["pcie_ceiling_path"] = ("concurrent pinned H2D + D2H of the step's bytes on two "
+                                        "streams, no kernel (same harness)")
+            del d_in, d_out
     sampler.stop()
     clocks = sampler.summary(t_wall0, t_wall1)
 
@@ -601,8 +630,8 @@ def main():
             "l2": "L2 flushed before every step (512 MiB write, then a 256 MiB read so "
                   "no dirty flush lines remain), outside the step's events" if need_flush else
                   f"working set {bytes_local // 2 >> 20} MiB per side > L2, no flush",
-            "tile_bits": _lib.get_tile_bits(E, inplace),
-            "tile_path": _lib.get_tile_path(E, inplace),
+            "tile_bits": None if args.workload == "cfg4-fft7" else chosen[0],
+            "tile_path": None if args.workload == "cfg4-fft7" else chosen[1],
         },
         "gelem_per_s": value / (2 * E),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -102,7 +102,8 @@ int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void
  * PCIe is full duplex, so with pinned host memory the per-array time tends
  * to max(H2D, D2H) instead of their sum.  host_dst[k] may equal host_src[k]
  * (in place on the host), and a host array may recur in the sequence: a copy
- * in waits for any in-flight copy out to the same host memory.  Ordered after prior work on `stream`; synchronous.
+ * in waits for any in-flight copy out to the same host memory.  Ordered after
+ * prior work on `stream`; synchronous.
  * dev_scratch: NULL (stream-ordered allocation) or 3 * batch * 2^b *
  * elem_bytes bytes.  No reference counterpart: the extension a caller with
  * many host arrays (the FFT pre-pass of BASELINE config 4) needs.
@@ -192,11 +193,24 @@ int bitrev_set_tile_bits(int elem_bytes, int inplace, int q);
  * on mbarriers), 2 = TMA tensor ring (one cp.async.bulk.tensor per tile),
  * 3 = rectangular register tiles (out of place only), 4 = element-granular
  * cp.async into the transposed layout (in place only).  Output never depends
- * on it; a (q, path) pair that is not instantiated falls back to path 0.  Initial value from the environment
- * (BITREV_B200_PATH_OOP / BITREV_B200_PATH_IP), else the measured default.
+ * on it; a (q, path) pair that is not instantiated falls back to path 0.
+ * Initial value from the environment (BITREV_B200_PATH_OOP /
+ * BITREV_B200_PATH_IP), else the measured default.
  */
 int bitrev_get_tile_path(int elem_bytes, int inplace);
 int bitrev_set_tile_path(int elem_bytes, int inplace, int path);
+
+/*
+ * The (tile bits, staging path) of the calling thread's most recent
+ * successful bitrev_oop / bitrev_inplace launch -- the choice tune_cobra's
+ * report names for the reference (src/bench.py:380-433).  path -1 = whole-row
+ * kernel (n*E <= 32 KB), -2 = element-wise kernel (unaligned views, 1/2-byte
+ * elements); q is 0 for both.  With the knobs at their defaults, launches
+ * moving at most 32 MiB per side (64 MiB in place) use smaller mid-size tiles:
+ * one large tile per SM leaves too few tiles to balance a persistent grid
+ * there (tools/mid_sizes.py).
+ */
+int bitrev_last_tile(int* q, int* path);
 
 /*
  * Tile visit order of the shared-memory kernels: 0 = middle value y equals

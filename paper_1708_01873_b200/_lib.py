@@ -42,6 +42,7 @@ SIGNATURES = {
     "bitrev_get_tile_order": (_c_int, [_c_int]),
     "bitrev_set_tile_order": (_c_int, [_c_int, _c_int]),
     "bitrev_launch_count": (_c_i64, []),
+    "bitrev_last_tile": (_c_int, [_vp, _vp]),
 }
 
 _lock = threading.Lock()
@@ -105,6 +106,14 @@ def get_tile_path(elem_bytes: int, inplace: bool) -> int:
 
 def set_tile_path(elem_bytes: int, inplace: bool, path: int) -> None:
     call("bitrev_set_tile_path", elem_bytes, int(inplace), path)
+
+
+def last_tile() -> tuple[int, int]:
+    """(tile bits, staging path) of this thread's most recent bitrev_oop /
+    bitrev_inplace launch; path -1 = whole-row kernel, -2 = element-wise."""
+    q, path = ctypes.c_int(0), ctypes.c_int(0)
+    call("bitrev_last_tile", ctypes.addressof(q), ctypes.addressof(path))
+    return q.value, path.value
 
 
 def get_tile_order(inplace: bool) -> int:

@@ -566,21 +566,50 @@ int check_common(int b, int E, int64_t batch) {
   return BITREV_OK;
 }
 
-int min_square_q(int E) { return E == 16 ? 3 : (E == 8 ? 4 : 5); }
-
-// Tile bits for (E, b, batch): the configured q, reduced so that 2q <= b and
-// -- for small problems -- until there are >= 8 tiles per SM to spread over
-// the grid (a 2^20-element array has only 256 Q=6 tiles for 148 SMs).  The
-// dispatchers then walk further down to the largest instantiated width.
-int pick_q(int E, int b, bool inplace, int64_t batch) {
-  int q = current_q(E, inplace);
-  while (q > 0 && 2 * q > b) --q;
-  static const int shrink = env_int("BITREV_B200_SHRINK", 0);  // measured: no gain (launch floor)
-  if (shrink) {
-    const uint64_t want = 8ull * (uint64_t)device_sms();
-    while (q > min_square_q(E) && ((uint64_t)batch << (b - 2 * q)) < want) --q;
+// Mid-size tile rule, measured on B200 (tools/mid_sizes.py ->
+// profiles/r01_mid_sizes.jsonl, event means over 80 flushed launches): up to a
+// per-side byte budget a persistent grid of one default tile per SM gets only
+// a few hundred tiles (1.7-3.5 waves), and smaller tiles with more resident
+// CTAs per SM balance it -- up to 1.28x (E=4, b=19, out of place), 1.23x
+// (E=8 in place, b=20), 1.16x (E=16 out of place, b=20).  Above the budget the
+// defaults win.  Returns 0 when the rule does not apply: the caller pinned the
+// tile bits or chose a non-default staging path, or the launch is large.
+int small_size_q(int E, bool inplace, uint64_t side_bytes) {
+  if (E != 4 && E != 8 && E != 16) return 0;
+  if ((inplace ? g_q_ip[E] : g_q_oop[E]).load() != 0) return 0;
+  if (tile_path(E, inplace) != default_path(E, inplace)) return 0;
+  uint64_t budget_mib = inplace ? 64 : 32;
+  int q = 0;
+  switch (E) {
+    case 4: q = 5; break;
+    case 8: q = 4; break;
+    case 16: q = inplace ? 0 : 5; break;  // in place the default Q=5 is already best
   }
+  return (q && side_bytes <= (budget_mib << 20)) ? q : 0;
+}
+
+uint64_t side_bytes(int E, int b, int64_t batch) { return ((uint64_t)E << b) * (uint64_t)batch; }
+
+// Tile bits for (E, b, batch): the mid-size rule or the configured q, reduced
+// so that 2q <= b.  The dispatchers then walk further down to the largest
+// instantiated width.
+int pick_q(int E, int b, bool inplace, int64_t batch) {
+  int q = small_size_q(E, inplace, side_bytes(E, b, batch));
+  if (!q) q = current_q(E, inplace);
+  while (q > 0 && 2 * q > b) --q;
   return q;
+}
+
+// The calling thread's most recent launch choice (bitrev_last_tile).
+thread_local int t_last_q = 0;
+thread_local int t_last_path = 0;
+
+int note(int rc, int q, int path) {
+  if (rc == BITREV_OK) {
+    t_last_q = q;
+    t_last_path = path;
+  }
+  return rc;
 }
 
 }  // namespace
@@ -622,30 +651,32 @@ int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
     if (s0 < d1 && d0 < s1) return BITREV_EOVERLAP;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (n * E <= kSmallBytes) return dispatch_small(E, src, dst, b, batch, src_batch_stride,
-                                                   dst_batch_stride, st);
+  if (n * E <= kSmallBytes)
+    return note(dispatch_small(E, src, dst, b, batch, src_batch_stride, dst_batch_stride, st), 0,
+                -1);
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
   if (vec_ok && (E == 4 || E == 8 || E == 16)) {
     // configured path first; every miss (shape not instantiated, b too small)
     // falls through to the square register tiles, then to the gather kernel
     const int path = tile_path(E, false);
-    if (path == 3) {
-      rc = dispatch_oop_rect(E, current_q(E, false), src, dst, b, batch, src_batch_stride,
-                             dst_batch_stride, st);
-      if (rc != BITREV_ETILE) return rc;
+    if (path == 3 && !small_size_q(E, false, side_bytes(E, b, batch))) {
+      const int qx = current_q(E, false);
+      rc = dispatch_oop_rect(E, qx, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
+      if (rc != BITREV_ETILE) return note(rc, qx, 3);
     }
     for (int q = pick_q(E, b, false, batch); q >= 3; --q) {
       if (path == 1 || path == 2) {
         rc = dispatch_ring(path, E, q, false, src, dst, b, batch, src_batch_stride,
                            dst_batch_stride, st);
-        if (rc != BITREV_ETILE) return rc;
+        if (rc != BITREV_ETILE) return note(rc, q, path);
       }
       rc = dispatch_oop_tile(E, q, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
-      if (rc != BITREV_ETILE) return rc;
+      if (rc != BITREV_ETILE) return note(rc, q, 0);
     }
   }
-  return dispatch_gather(E, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
+  return note(dispatch_gather(E, src, dst, b, batch, src_batch_stride, dst_batch_stride, st), 0,
+              -2);
 }
 
 int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_stride,
@@ -658,24 +689,25 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
   if (batch > 1 && batch_stride < n) return BITREV_EBATCH;
   if (batch == 1) batch_stride = n;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (n * E <= kSmallBytes) return dispatch_small(E, a, a, b, batch, batch_stride, batch_stride, st);
+  if (n * E <= kSmallBytes)
+    return note(dispatch_small(E, a, a, b, batch, batch_stride, batch_stride, st), 0, -1);
   const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
   if (vec_ok && (E == 4 || E == 8 || E == 16)) {
     const int path = tile_path(E, true);
     for (int q = pick_q(E, b, true, batch); q >= 3; --q) {
       if (path == 4) {
         rc = dispatch_ip_cpa(E, q, a, b, batch, batch_stride, st);
-        if (rc != BITREV_ETILE) return rc;
+        if (rc != BITREV_ETILE) return note(rc, q, 4);
       }
       if (path == 1 || path == 2) {
         rc = dispatch_ring(path, E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
-        if (rc != BITREV_ETILE) return rc;
+        if (rc != BITREV_ETILE) return note(rc, q, path);
       }
       rc = dispatch_ip_tile(E, q, a, b, batch, batch_stride, st);
-      if (rc != BITREV_ETILE) return rc;
+      if (rc != BITREV_ETILE) return note(rc, q, 0);
     }
   }
-  return dispatch_swap(E, a, b, batch, batch_stride, st);
+  return note(dispatch_swap(E, a, b, batch, batch_stride, st), 0, -2);
 }
 
 int bitrev_oop_host(const void* host_src, void* host_dst, int b, int elem_bytes, int64_t batch,
@@ -1063,6 +1095,13 @@ int bitrev_set_tile_path(int elem_bytes, int inplace, int path) {
   if (path < 0 || path > 4 || (path == 3 && inplace) || (path == 4 && !inplace))
     return BITREV_ETILE;
   (inplace ? g_path_ip : g_path_oop)[elem_bytes].store(path);
+  return BITREV_OK;
+}
+
+int bitrev_last_tile(int* q, int* path) {
+  if (!q || !path) return BITREV_ENULL;
+  *q = t_last_q;
+  *path = t_last_path;
   return BITREV_OK;
 }
 
