@@ -33,7 +33,7 @@ std::atomic<int> g_q_ip[17];
 // (E, family).
 int default_q(int E, bool inplace) {
   switch (E) {
-    case 4: return inplace ? 6 : 7;
+    case 4: return inplace ? 6 : 8;   // out of place: rectangular QX = 8 (path 3)
     case 8: return inplace ? 6 : 7;   // out of place: rectangular QX = 7 (path 3)
     case 16: return inplace ? 5 : 6;
     default: return 0;
@@ -73,8 +73,9 @@ std::atomic<int> g_path_ip[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1
 int default_path(int E, bool inplace) {
   if (inplace) return 0;  // register tile pairs (compact pair enumeration)
   switch (E) {
+    case 4:
     case 8: return 3;     // rectangular register tiles (1 KB destination rows)
-    default: return 0;    // register tiles
+    default: return 0;    // square register tiles (E=16: 1 KB rows both sides)
   }
 }
 
@@ -404,27 +405,33 @@ int launch_oop_rect(const void* src, void* dst, int b, int64_t batch, int64_t sb
   return finish_launch();
 }
 
-// q selects the destination run (QX); QZ is the 128-byte source piece.
+// Rectangular tiles: q selects the destination run (QX elements), rect_qz the
+// source piece (QZ elements).  Measured on B200 (tools/rect_qz.py ->
+// profiles/r01_rect_qz.jsonl, b = 26/28/30): 1 KB destination rows with
+// 256-byte source pieces win -- E=8 (7,5) 6.17 TB/s vs (7,4) 5.91; E=4 (8,6)
+// 6.22 vs square Q7 6.00.  BITREV_B200_RECT_QZ overrides QZ for every QX
+// (experiments; shapes outside the table below fall back to square tiles).
+int rect_qz(int E, int qx) {
+  static const int env = env_int("BITREV_B200_RECT_QZ", 0);
+  if (env) return env;
+  switch (E) {
+    case 4: return qx >= 7 ? 6 : 5;
+    case 8: return qx >= 6 ? 5 : 4;
+    case 16: return qx >= 6 ? 4 : 3;
+  }
+  return 0;
+}
+
 int dispatch_oop_rect(int E, int q, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
                       int64_t dbs, cudaStream_t st) {
-  switch (E) {
-    case 4:
-      if (q == 6) return launch_oop_rect<4, 6, 5>(src, dst, b, batch, sbs, dbs, st);
-      if (q == 7) return launch_oop_rect<4, 7, 5>(src, dst, b, batch, sbs, dbs, st);
-      if (q == 8) return launch_oop_rect<4, 8, 5>(src, dst, b, batch, sbs, dbs, st);
-      break;
-    case 8:
-      if (q == 5) return launch_oop_rect<8, 5, 4>(src, dst, b, batch, sbs, dbs, st);
-      if (q == 6) return launch_oop_rect<8, 6, 4>(src, dst, b, batch, sbs, dbs, st);
-      if (q == 7) return launch_oop_rect<8, 7, 4>(src, dst, b, batch, sbs, dbs, st);
-      break;
-    case 16:
-      if (q == 4) return launch_oop_rect<16, 4, 3>(src, dst, b, batch, sbs, dbs, st);
-      if (q == 5) return launch_oop_rect<16, 5, 3>(src, dst, b, batch, sbs, dbs, st);
-      if (q == 6) return launch_oop_rect<16, 6, 3>(src, dst, b, batch, sbs, dbs, st);
-      if (q == 7) return launch_oop_rect<16, 7, 3>(src, dst, b, batch, sbs, dbs, st);
-      break;
-  }
+  const int qz = rect_qz(E, q);
+#define RECT(EE, QX, QZ)                                                       \
+  if (E == EE && q == QX && qz == QZ)                                          \
+    return launch_oop_rect<EE, QX, QZ>(src, dst, b, batch, sbs, dbs, st);
+  RECT(4, 6, 5) RECT(4, 7, 6) RECT(4, 8, 6)
+  RECT(8, 5, 4) RECT(8, 6, 5) RECT(8, 7, 5)
+  RECT(16, 4, 3) RECT(16, 5, 3) RECT(16, 6, 4) RECT(16, 7, 4)
+#undef RECT
   return BITREV_ETILE;
 }
 
@@ -566,36 +573,47 @@ int check_common(int b, int E, int64_t batch) {
   return BITREV_OK;
 }
 
-// Mid-size tile rule, measured on B200 (tools/mid_sizes.py ->
-// profiles/r01_mid_sizes.jsonl, event means over 80 flushed launches): up to a
-// per-side byte budget a persistent grid of one default tile per SM gets only
-// a few hundred tiles (1.7-3.5 waves), and smaller tiles with more resident
-// CTAs per SM balance it -- up to 1.28x (E=4, b=19, out of place), 1.23x
-// (E=8 in place, b=20), 1.16x (E=16 out of place, b=20).  Above the budget the
-// defaults win.  Returns 0 when the rule does not apply: the caller pinned the
-// tile bits or chose a non-default staging path, or the launch is large.
-int small_size_q(int E, bool inplace, uint64_t side_bytes) {
-  if (E != 4 && E != 8 && E != 16) return 0;
-  if ((inplace ? g_q_ip[E] : g_q_oop[E]).load() != 0) return 0;
-  if (tile_path(E, inplace) != default_path(E, inplace)) return 0;
-  uint64_t budget_mib = inplace ? 64 : 32;
-  int q = 0;
-  switch (E) {
-    case 4: q = 5; break;
-    case 8: q = 4; break;
-    case 16: q = inplace ? 0 : 5; break;  // in place the default Q=5 is already best
+// Mid-size tile tiers, measured on B200 (tools/mid_sizes.py ->
+// profiles/r01_mid_sizes.jsonl, event means over 80 flushed launches): up to
+// a per-side byte budget a persistent grid of one default tile per SM gets
+// only a few hundred tiles (1.7-3.5 waves), and smaller tiles with more
+// resident CTAs per SM balance it -- up to 1.28x (E=4, b=19, out of place),
+// 1.23x (E=8 in place, b=20), 1.16x (E=16 out of place, b=20), 1.07x (E=8
+// out of place, b=22).  Above the last budget the defaults win.
+struct Tier {
+  int q = 0, path = 0;  // q = 0: no tier applies
+};
+
+Tier mid_tier(int E, bool inplace, uint64_t side_bytes) {
+  Tier t;
+  if (E != 4 && E != 8 && E != 16) return t;
+  // Knobs compare by value, so saving a knob and setting it back keeps the
+  // tiers; any other value switches them off.
+  if (current_q(E, inplace) != default_q(E, inplace)) return t;
+  if (tile_path(E, inplace) != default_path(E, inplace)) return t;
+  const uint64_t mib = side_bytes >> 20, exact = side_bytes & ((1u << 20) - 1);
+  auto within = [&](uint64_t budget_mib) { return mib < budget_mib || (mib == budget_mib && !exact); };
+  if (E == 4 && !inplace) {
+    if (within(32)) t = {5, 0};       // square Q5 up to b = 23
+    else if (within(64)) t = {7, 3};  // rectangular QX = 7 (512 B rows) at b = 24
+  } else if (E == 4 && inplace) {
+    if (within(64)) t = {5, 0};
+  } else if (E == 8 && !inplace) {
+    if (within(32)) t = {4, 0};       // square Q4 up to b = 22
+  } else if (E == 8 && inplace) {
+    if (within(64)) t = {4, 0};
+  } else if (E == 16 && !inplace) {
+    if (within(32)) t = {5, 0};
   }
-  return (q && side_bytes <= (budget_mib << 20)) ? q : 0;
+  return t;
 }
 
 uint64_t side_bytes(int E, int b, int64_t batch) { return ((uint64_t)E << b) * (uint64_t)batch; }
 
-// Tile bits for (E, b, batch): the mid-size rule or the configured q, reduced
-// so that 2q <= b.  The dispatchers then walk further down to the largest
+// Tile bits for the square kernels: the configured q, reduced so that
+// 2q <= b.  The dispatchers then walk further down to the largest
 // instantiated width.
-int pick_q(int E, int b, bool inplace, int64_t batch) {
-  int q = small_size_q(E, inplace, side_bytes(E, b, batch));
-  if (!q) q = current_q(E, inplace);
+int clamp_q(int q, int b) {
   while (q > 0 && 2 * q > b) --q;
   return q;
 }
@@ -659,13 +677,17 @@ int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
   if (vec_ok && (E == 4 || E == 8 || E == 16)) {
     // configured path first; every miss (shape not instantiated, b too small)
     // falls through to the square register tiles, then to the gather kernel
-    const int path = tile_path(E, false);
-    if (path == 3 && !small_size_q(E, false, side_bytes(E, b, batch))) {
-      const int qx = current_q(E, false);
-      rc = dispatch_oop_rect(E, qx, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
-      if (rc != BITREV_ETILE) return note(rc, qx, 3);
+    int path = tile_path(E, false), q0 = current_q(E, false);
+    const Tier t = mid_tier(E, false, side_bytes(E, b, batch));
+    if (t.q) {
+      q0 = t.q;
+      path = t.path;
     }
-    for (int q = pick_q(E, b, false, batch); q >= 3; --q) {
+    if (path == 3) {
+      rc = dispatch_oop_rect(E, q0, src, dst, b, batch, src_batch_stride, dst_batch_stride, st);
+      if (rc != BITREV_ETILE) return note(rc, q0, 3);
+    }
+    for (int q = clamp_q(q0, b); q >= 3; --q) {
       if (path == 1 || path == 2) {
         rc = dispatch_ring(path, E, q, false, src, dst, b, batch, src_batch_stride,
                            dst_batch_stride, st);
@@ -694,7 +716,8 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
   const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
   if (vec_ok && (E == 4 || E == 8 || E == 16)) {
     const int path = tile_path(E, true);
-    for (int q = pick_q(E, b, true, batch); q >= 3; --q) {
+    const Tier t = mid_tier(E, true, side_bytes(E, b, batch));
+    for (int q = clamp_q(t.q ? t.q : current_q(E, true), b); q >= 3; --q) {
       if (path == 4) {
         rc = dispatch_ip_cpa(E, q, a, b, batch, batch_stride, st);
         if (rc != BITREV_ETILE) return note(rc, q, 4);

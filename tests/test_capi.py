@@ -59,7 +59,7 @@ def test_error_codes_without_gpu():
 
 
 def test_tile_bits_registry():
-    for E, q_oop, q_ip in ((4, 7, 6), (8, 7, 6), (16, 6, 5)):
+    for E, q_oop, q_ip in ((4, 8, 6), (8, 7, 6), (16, 6, 5)):
         assert _lib.get_tile_bits(E, False) == q_oop
         assert _lib.get_tile_bits(E, True) == q_ip
     _lib.set_tile_bits(8, True, 4)

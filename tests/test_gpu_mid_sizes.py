@@ -1,9 +1,9 @@
-"""Mid-size tile rule (bitrev_capi.cu small_size_q, measured by
-tools/mid_sizes.py): with default knobs, launches moving at most 32 MiB per
-side (64 MiB in place) use smaller tiles; one width above the budget they use
-the large-size defaults; pinned knobs switch the rule off.  Every case is also
-byte-compared with the oracle, so the mid-size tiles are parity-covered at the
-very sizes where they run.
+"""Mid-size tile tiers (bitrev_capi.cu mid_tier, measured by
+tools/mid_sizes.py): with default knobs, launches below per-family byte
+budgets use smaller tiles, and one width above the last budget the large-size
+defaults; a non-default knob value switches the tiers off.  Every case is
+also byte-compared with the oracle, so the mid-size tiles are parity-covered
+at the very sizes where they run.
 """
 
 import numpy as np
@@ -16,10 +16,21 @@ from oracle import oracle as orc
 pytestmark = pytest.mark.gpu
 
 NP = {4: np.int32, 8: np.int64, 16: np.complex128}
-# (E, inplace) -> (mid-size q, budget MiB per side, large-size (q, path))
-RULE = {(4, False): (5, 32, (7, 0)), (4, True): (5, 64, (6, 0)),
-        (8, False): (4, 32, (7, 3)), (8, True): (4, 64, (6, 0)),
-        (16, False): (5, 32, (6, 0)), (16, True): (5, 64, (5, 0))}
+# (E, inplace) -> default (q, path) above every budget
+LARGE = {(4, False): (8, 3), (4, True): (6, 0), (8, False): (7, 3), (8, True): (6, 0),
+         (16, False): (6, 0), (16, True): (5, 0)}
+# (E, inplace, b, expected (q, path)) at each budget and one width above it
+CASES = [
+    (4, False, 23, (5, 0)), (4, False, 24, (7, 3)),    # 32 MiB tier: square Q5
+    (4, False, 25, (8, 3)),                            # above the 64 MiB rect QX=7 tier
+    (4, True, 24, (5, 0)), (4, True, 25, (6, 0)),
+    (8, False, 22, (4, 0)), (8, False, 23, (7, 3)),
+    (8, True, 23, (4, 0)), (8, True, 24, (6, 0)),
+    (16, False, 21, (5, 0)), (16, False, 22, (6, 0)),
+    (16, True, 22, (5, 0)), (16, True, 23, (5, 0)),    # no tier (default Q5)
+]
+# pinned values that differ from the default and from any tier's q
+PIN = {(4, False): 6, (4, True): 7, (8, False): 6, (8, True): 5, (16, False): 4, (16, True): 4}
 
 
 def rand_bits(n, E, seed):
@@ -39,36 +50,32 @@ def run(host, b, inplace, cuda):
     return out.cpu().numpy(), br.last_tile()
 
 
-def budget_width(E, mib):
-    return (mib << 20).bit_length() - 1 - (E.bit_length() - 1)
-
-
-@pytest.mark.parametrize("E,inplace", sorted(RULE))
-@pytest.mark.parametrize("above", [False, True])
-def test_mid_size_rule_and_parity(cuda, E, inplace, above):
-    q_mid, mib, large = RULE[(E, inplace)]
-    b = budget_width(E, mib) + int(above)
-    assert (E << b) == (mib << 20) << int(above)
+@pytest.mark.parametrize("E,inplace,b,expected", CASES)
+def test_mid_size_tiers_and_parity(cuda, E, inplace, b, expected):
     host = rand_bits(1 << b, E, seed=E * 100 + b)
     got, choice = run(host, b, inplace, cuda)
-    assert choice == (large if above else (q_mid, 0))
+    assert choice == expected
     assert np.array_equal(got.view(np.uint8), orc.oracle_permute(host, b).view(np.uint8))
 
 
-@pytest.mark.parametrize("E,inplace", sorted(RULE))
-def test_pinned_tile_bits_disable_the_rule(cuda, E, inplace):
-    _, mib, (q_large, _) = RULE[(E, inplace)]
-    b = budget_width(E, mib) - 2
-    q_pin = 6 if E != 16 else 4
+@pytest.mark.parametrize("E,inplace", sorted(LARGE))
+def test_pinned_tile_bits_disable_the_tiers(cuda, E, inplace):
+    """Tile bits set to a non-default value switch the tiers off; setting the
+    default value back (save/restore) switches them on again."""
+    b = 20
     old = br.get_tile_bits(E, inplace)
-    br.set_tile_bits(E, inplace, q_pin)
+    assert old == LARGE[(E, inplace)][0]
+    br.set_tile_bits(E, inplace, PIN[(E, inplace)])
     try:
         host = rand_bits(1 << b, E, seed=E * 300 + b)
         got, (q, _) = run(host, b, inplace, cuda)
     finally:
-        br.set_tile_bits(E, inplace, 0)
-    assert old == q_large and q == q_pin
+        br.set_tile_bits(E, inplace, old)  # by value: the default again
+    assert q == PIN[(E, inplace)]
     assert np.array_equal(got.view(np.uint8), orc.oracle_permute(host, b).view(np.uint8))
+    _, choice = run(host, b, inplace, cuda)
+    small = min((c for c in CASES if c[:2] == (E, inplace)), key=lambda c: c[2])
+    assert choice == small[3]  # b=20 sits in the lowest tier (or the default)
 
 
 def test_last_tile_reports_row_and_elementwise_kernels(cuda):

@@ -66,6 +66,8 @@ def main():
                 cands = [(q, 0) for q in (QS_IP if inplace else QS_OOP)[E]]
                 if E == 8 and not inplace:
                     cands += [(7, 3), (6, 3)]
+                if E == 4 and not inplace:
+                    cands += [(8, 3), (7, 3)]
                 for q, p in cands:
                     if 2 * q > b:
                         continue
