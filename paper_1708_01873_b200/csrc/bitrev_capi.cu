@@ -973,6 +973,11 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     if (s0 < d1 && d0 < s1) return BITREV_EOVERLAP;
   }
   if (stages < 0 || stages > b) return BITREV_ESTAGES;
+  // No butterflies: the plain permutation kernels are faster than the
+  // butterfly tiles with zero stages (6.43 vs 5.32 TB/s complex128, 6.32 vs
+  // 6.02 complex64, profiles/r01_fft_qz_ab.txt).
+  if (stages == 0)
+    return bitrev_oop(src, dst, b, E, batch, src_batch_stride, dst_batch_stride, stream);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   FftArgs fa;
   memset(&fa, 0, sizeof fa);
@@ -1000,8 +1005,15 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   // Fused path: rectangular tiles whose destination rows are the FFT blocks
   // (complex64: QX = 7, 128-element rows, up to 7 stages; complex128: QX = 6,
   // 64-element rows, up to 6 stages).  Rows too big for the small kernel are
-  // always wide enough (b >= 13 resp. 12 > QX + QZ).
-  const int qx = E == 8 ? 7 : 6, qz = E == 8 ? 4 : 3;
+  // always wide enough (b >= 13 resp. 12 >= QX + QZ).
+  // QZ (source pieces) per (E, stages), measured (tools/fft_stage_sweep.py,
+  // profiles/r01_fft_qz_ab.txt).  complex128 with 128-byte pieces has 8 rows
+  // per tile, and with 2 rows per warp pass half the warps idle in the
+  // butterfly drain; 256-byte pieces (16 rows) keep all 8 busy: +29 % at 4
+  // stages, +16 % at 6, -2.5 % at 1.  complex64 with 256-byte pieces needs
+  // ~165 registers (1 CTA/SM): it only pays at 7 stages (+2.4 %).
+  const bool wide = E == 8 ? stages == 7 : stages >= 2;
+  const int qx = E == 8 ? 7 : 6, qz = (E == 8 ? 4 : 3) + (wide ? 1 : 0);
   if (stages > qx || b < qx + qz) return BITREV_ESTAGES;
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
@@ -1018,15 +1030,15 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   }
   if (E == 8) {
     switch (stages) {
-      FFT_LAUNCH(8, 7, 4, 0) FFT_LAUNCH(8, 7, 4, 1) FFT_LAUNCH(8, 7, 4, 2)
+      FFT_LAUNCH(8, 7, 4, 1) FFT_LAUNCH(8, 7, 4, 2)
       FFT_LAUNCH(8, 7, 4, 3) FFT_LAUNCH(8, 7, 4, 4) FFT_LAUNCH(8, 7, 4, 5)
-      FFT_LAUNCH(8, 7, 4, 6) FFT_LAUNCH(8, 7, 4, 7)
+      FFT_LAUNCH(8, 7, 4, 6) FFT_LAUNCH(8, 7, 5, 7)
     }
   } else {
     switch (stages) {
-      FFT_LAUNCH(16, 6, 3, 0) FFT_LAUNCH(16, 6, 3, 1) FFT_LAUNCH(16, 6, 3, 2)
-      FFT_LAUNCH(16, 6, 3, 3) FFT_LAUNCH(16, 6, 3, 4) FFT_LAUNCH(16, 6, 3, 5)
-      FFT_LAUNCH(16, 6, 3, 6)
+      FFT_LAUNCH(16, 6, 3, 1) FFT_LAUNCH(16, 6, 4, 2)
+      FFT_LAUNCH(16, 6, 4, 3) FFT_LAUNCH(16, 6, 4, 4) FFT_LAUNCH(16, 6, 4, 5)
+      FFT_LAUNCH(16, 6, 4, 6)
     }
   }
 #undef FFT_LAUNCH

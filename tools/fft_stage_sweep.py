@@ -1,4 +1,7 @@
-"""GB/s of the fused FFT pre-pass vs number of fused stages (cfg4 shape)."""
+"""GB/s of the fused FFT pre-pass vs number of fused stages (cfg4 shape:
+4096 rows of 2^16; --c128 for 2048 complex128 rows).  The A/B of 128- vs
+256-byte source pieces that set the per-stage tile shapes ran with an
+environment switch that has since been removed: profiles/r01_fft_qz_ab.txt."""
 import sys
 from pathlib import Path
 
@@ -6,10 +9,13 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1708_01873_b200 import _core, _lib  # noqa: E402
-import paper_1708_01873_b200 as br  # noqa: E402
 
-b, rows = 16, 4096
-x = torch.empty((rows, 1 << b), dtype=torch.complex64, device="cuda").normal_()
+C128 = "--c128" in sys.argv
+E = 16 if C128 else 8
+b, rows = 16, 4096 if not C128 else 2048
+x = torch.empty((rows, 1 << b), dtype=torch.complex128 if C128 else torch.complex64,
+                device="cuda").normal_()
+tag = f"E={E}"
 y = torch.empty_like(x)
 st = torch.cuda.current_stream().cuda_stream
 
@@ -23,14 +29,12 @@ def t(fn, reps=20):
         fn()
     e.record()
     e.synchronize()
-    return 2 * x.numel() * 8 * reps / (s.elapsed_time(e) / 1e3) / 1e9
+    return 2 * x.numel() * E * reps / (s.elapsed_time(e) / 1e3) / 1e9
 
 
-for stages in (0, 1, 2, 4, 6, 7):
-    gbs = t(lambda: _lib.call("bitrev_dit_prepass", x.data_ptr(), y.data_ptr(), b, 8, rows,
+for stages in (0, 1, 2, 4, 6, 7) if E == 8 else (0, 1, 2, 4, 6):
+    gbs = t(lambda: _lib.call("bitrev_dit_prepass", x.data_ptr(), y.data_ptr(), b, E, rows,
                               1 << b, 1 << b, stages, 0, st))
-    print(f"fft rect stages={stages}: {gbs:.0f} GB/s")
-for path, q in ((0, 6), (1, 6), (3, 7)):
-    br.set_tile_bits(8, False, q)
-    br.set_tile_path(8, False, path)
-    print(f"plain bitrev path={path} q={q}: {t(lambda: _core.launch_oop(x, y, b)):.0f} GB/s")
+    print(f"{tag} fft rect stages={stages}: {gbs:.0f} GB/s")
+print(f"{tag} plain bitrev (default tiles {_lib.get_tile_bits(E, False)}/"
+      f"{_lib.get_tile_path(E, False)}): {t(lambda: _core.launch_oop(x, y, b)):.0f} GB/s")
