@@ -192,7 +192,8 @@ int bitrev_set_tile_bits(int elem_bytes, int inplace, int q);
  * (cp.async.bulk row copies into a multi-stage shared-memory ring completing
  * on mbarriers), 2 = TMA tensor ring (one cp.async.bulk.tensor per tile),
  * 3 = rectangular register tiles (out of place only), 4 = element-granular
- * cp.async into the transposed layout (in place only).  Output never depends
+ * cp.async into the transposed layout (in place only), 5 = register loads +
+ * TMA tensor stores from a swizzled staging buffer (in place only).  Output never depends
  * on it; a (q, path) pair that is not instantiated falls back to path 0.
  * Initial value from the environment (BITREV_B200_PATH_OOP /
  * BITREV_B200_PATH_IP), else the measured default.

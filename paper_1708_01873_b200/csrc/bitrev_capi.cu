@@ -323,6 +323,41 @@ bool encode_tile_map(CUtensorMap* map, const void* base, int b, int E, int q, in
   return r == CUDA_SUCCESS;
 }
 
+// In-place tile pairs with TMA tensor stores (path 5): compact pairs only.
+template <int E, int Q>
+int launch_ip_tstore(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  using S = TsTile<E, Q>;
+  if (S::SMEM > 227 * 1024) return BITREV_ETILE;
+  CUtensorMap map;
+  memset(&map, 0, sizeof map);
+  if (!encode_tile_map(&map, buf, b, E, Q, batch, bs)) return BITREV_ETILE;
+  auto kern = bitrev_inplace_tstore_kernel<E, Q>;
+  const int per_sm = prepare_kernel(kern, Tile<E, Q>::THREADS, S::SMEM);
+  TileArgs a;
+  memset(&a, 0, sizeof a);
+  a.src = static_cast<const char*>(buf);
+  a.dst = static_cast<char*>(buf);
+  a.b = b;
+  a.m = b - 2 * Q;
+  a.src_bstride = bs * E;
+  a.dst_bstride = bs * E;
+  a.order = 2;
+  const int grid = set_pair_work(a, batch, true, per_sm);
+  kern<<<grid, Tile<E, Q>::THREADS, S::SMEM, st>>>(map, a);
+  return finish_launch();
+}
+
+int dispatch_ip_tstore(int E, int q, void* buf, int b, int64_t batch, int64_t bs,
+                       cudaStream_t st) {
+  if (2 * q > b) return BITREV_ETILE;
+  if (E == 4 && q == 6) return launch_ip_tstore<4, 6>(buf, b, batch, bs, st);
+  if (E == 8 && q == 5) return launch_ip_tstore<8, 5>(buf, b, batch, bs, st);
+  if (E == 8 && q == 6) return launch_ip_tstore<8, 6>(buf, b, batch, bs, st);
+  if (E == 16 && q == 4) return launch_ip_tstore<16, 4>(buf, b, batch, bs, st);
+  if (E == 16 && q == 5) return launch_ip_tstore<16, 5>(buf, b, batch, bs, st);
+  return BITREV_ETILE;
+}
+
 template <int E, int Q, bool INPLACE, int MODE, bool COMPACT>
 int launch_ring_mode(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
                      cudaStream_t st) {
@@ -721,6 +756,10 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
       if (path == 4) {
         rc = dispatch_ip_cpa(E, q, a, b, batch, batch_stride, st);
         if (rc != BITREV_ETILE) return note(rc, q, 4);
+      }
+      if (path == 5) {
+        rc = dispatch_ip_tstore(E, q, a, b, batch, batch_stride, st);
+        if (rc != BITREV_ETILE) return note(rc, q, 5);
       }
       if (path == 1 || path == 2) {
         rc = dispatch_ring(path, E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
@@ -1127,7 +1166,7 @@ int bitrev_get_tile_path(int elem_bytes, int inplace) { return tile_path(elem_by
 
 int bitrev_set_tile_path(int elem_bytes, int inplace, int path) {
   if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16) return BITREV_ETILE;
-  if (path < 0 || path > 4 || (path == 3 && inplace) || (path == 4 && !inplace))
+  if (path < 0 || path > 5 || (path == 3 && inplace) || (path >= 4 && !inplace))
     return BITREV_ETILE;
   (inplace ? g_path_ip : g_path_oop)[elem_bytes].store(path);
   return BITREV_OK;

@@ -863,6 +863,144 @@ __global__ void __launch_bounds__(Ring<E, Q, INPLACE, MODE>::THREADS)
 }
 
 // ---------------------------------------------------------------------------
+// in-place tile pairs with TMA tensor stores (path 5)
+//
+// Loads are the register kernel's (LDG.128 of whole 2^Q*E-byte rows), but the
+// lanes of a warp take a row's 16-byte chunks in bit-reversed order,
+// c = rev(l).  After the V x V register transpose, chunk (c, J) belongs to
+// destination row x' = rev_Q(c*V + J) = rev_LV(J)*CH + l, so the STS go
+// straight into the SWIZZLE_128B layout of the tensor map's box (segment
+// piece*2^Q + x', 16-byte chunk cc at cc ^ (x' & 7)) and the eight lanes of a
+// quarter warp land on eight different x' mod 8: conflict-free.  One elected
+// thread then stores each staged tile with cp.async.bulk.tensor (global <-
+// shared) through the same 5-D map the tensor ring loads with.  There is no
+// LDS/STG drain: the threads go straight on to the next pair's loads while
+// the TMA engine writes.  Two pair slots: slot k%2 is restaged only after the
+// bulk group that read it (pair k-2) has finished reading shared memory.
+
+template <int E, int Q>
+struct TsTile {
+  using T = Tile<E, Q>;
+  static constexpr int LCH = const_log2(T::CH);
+  static constexpr int TILE = T::BYTES;
+  static constexpr int SLOT = 2 * TILE;
+  static constexpr int SMEM = 2 * SLOT + 1024;  // + slack for 1024-B alignment
+  static_assert(((1 << Q) * E) % 128 == 0, "tensor tiles need 128-byte rows");
+};
+
+__device__ __forceinline__ void tma_store_5d(const void* tmap, uint32_t src, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group"
+      " [%0, {%1, %1, %1, %2, %3}], [%4];" ::"l"(tmap),
+      "r"(0), "r"(c3), "r"(c4), "r"(src)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <int E, int Q>
+__device__ __forceinline__ void ts_load(uint4 (&r)[Tile<E, Q>::IPT][Tile<E, Q>::V],
+                                        const char* tile_base, uint64_t row_stride) {
+  using T = Tile<E, Q>;
+  using S = TsTile<E, Q>;
+#pragma unroll
+  for (int it = 0; it < T::IPT; ++it) {
+    const int id = it * T::THREADS + threadIdx.x;
+    const int c = (int)(__brev((unsigned)(id % T::CH)) >> (32 - S::LCH));
+    const int g = id / T::CH;
+#pragma unroll
+    for (int k = 0; k < T::V; ++k) {
+      const char* p = tile_base + (uint64_t)(g + k * T::CH) * row_stride + (uint64_t)c * 16;
+      r[it][k] = BITREV_IP_NC ? ld_stream(p) : ld_plain(p);
+    }
+  }
+}
+
+template <int E, int Q, int J>
+__device__ __forceinline__ void ts_stage_col(const uint4 (&a)[16 / E], uint32_t tile, int l,
+                                             int piece, int cc) {
+  using T = Tile<E, Q>;
+  if constexpr (J < T::V) {
+    constexpr int RJ = T::V == 1 ? 0 : (T::V == 2 ? J : ((J & 1) << 1) | (J >> 1));  // rev_LV(J)
+    const int xr = l + RJ * T::CH;  // destination row
+    sts128(tile + (uint32_t)(((piece << Q) + xr) * 128 + ((cc ^ (xr & 7)) << 4)), xpose<E, J>(a));
+    ts_stage_col<E, Q, J + 1>(a, tile, l, piece, cc);
+  }
+}
+
+template <int E, int Q>
+__device__ __forceinline__ void ts_stage(const uint4 (&r)[Tile<E, Q>::IPT][Tile<E, Q>::V],
+                                         uint32_t tile) {
+  using T = Tile<E, Q>;
+#pragma unroll
+  for (int it = 0; it < T::IPT; ++it) {
+    const int id = it * T::THREADS + threadIdx.x;
+    const int l = id % T::CH;
+    const int g = id / T::CH;
+    const int ch = (int)(__brev((unsigned)g) >> (32 - (Q - T::LV)));  // destination chunk
+    ts_stage_col<E, Q, 0>(r[it], tile, l, ch >> 3, ch & 7);
+  }
+}
+
+template <int E, int Q>
+__global__ void __launch_bounds__(Tile<E, Q>::THREADS, 1)
+    bitrev_inplace_tstore_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs a) {
+  using T = Tile<E, Q>;
+  using S = TsTile<E, Q>;
+  extern __shared__ __align__(1024) unsigned char smem_ts[];
+  const uint32_t base = (smem_u32(smem_ts) + 1023u) & ~1023u;
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  uint4 r0[T::IPT][T::V], r1[T::IPT][T::V];
+  PairCursor pc;
+  pc.start(a);
+  if (!pc.valid(a)) return;
+  auto issue = [&]() {
+    const uint64_t y = pair_from_index(pc.w, a.m), ry = dev_rev(y, a.m);
+    const char* b0 = a.src + pc.bi * a.src_bstride;
+    ts_load<E, Q>(r0, b0 + (y << Q) * E, row_stride);
+    if (ry != y) ts_load<E, Q>(r1, b0 + (ry << Q) * E, row_stride);
+  };
+  issue();
+  for (int k = 0;; ++k) {
+    const uint64_t bi = pc.bi, y = pair_from_index(pc.w, a.m), ry = dev_rev(y, a.m);
+    const bool pair = ry != y;
+    const uint32_t slot = base + (uint32_t)((k & 1) * S::SLOT);
+    if (threadIdx.x == 0) bulk_wait_read<1>();  // pair k-2's stores have read this slot
+    __syncthreads();
+    ts_stage<E, Q>(r0, slot);
+    if (pair) ts_stage<E, Q>(r1, slot + S::TILE);
+    fence_async_smem();  // generic-proxy STS -> visible to the async proxy
+    __syncthreads();
+    pc.next(a);
+    const bool more = pc.valid(a);
+    if (more) issue();
+    if (threadIdx.x == 0) {
+      tma_store_5d(&tmap, slot, (int)ry, (int)bi);  // tile y's data into slab rev(y)
+      if (pair) tma_store_5d(&tmap, slot + S::TILE, (int)y, (int)bi);
+      bulk_commit();
+    }
+    if (!more) break;
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
 // in-place tile pairs through cp.async (LDGSTS) straight into the transposed
 // layout
 //

@@ -77,11 +77,11 @@ def test_every_tile_size(cuda, E, b):
     try:
         for q in qs:
             for order in (0, 1, 2):
-                for path in (0, 1, 2, 4):
+                for path in (0, 1, 2, 4, 5):
                     for inplace in (False, True):
                         br.set_tile_bits(E, inplace, q)
                         br.set_tile_order(inplace, order)
-                        br.set_tile_path(E, inplace, path if (inplace or path != 4) else 0)
+                        br.set_tile_path(E, inplace, path if (inplace or path < 4) else 0)
                     src = torch.from_numpy(host).to(cuda)
                     dst = torch.empty_like(src)
                     br.cobra_out_of_place(src, dst, br.CobraConfig(0), b)
@@ -117,7 +117,7 @@ def test_rect_out_of_place_tiles(cuda, E, q, b, batch):
 
 
 @pytest.mark.parametrize("order", [0, 2])
-@pytest.mark.parametrize("path", [0, 1, 2, 4])
+@pytest.mark.parametrize("path", [0, 1, 2, 4, 5])
 @pytest.mark.parametrize("E", [4, 8, 16])
 @pytest.mark.parametrize("b,batch", [(12, 2), (13, 3), (14, 3), (15, 5), (19, 2), (22, 1)])
 def test_both_staging_paths(cuda, order, path, E, b, batch):
@@ -131,7 +131,7 @@ def test_both_staging_paths(cuda, order, path, E, b, batch):
     try:
         br.set_tile_order(False, order)
         br.set_tile_order(True, order)
-        br.set_tile_path(E, False, path if path != 4 else 0)
+        br.set_tile_path(E, False, path if path < 4 else 0)
         br.set_tile_path(E, True, path)
         src = torch.from_numpy(host).to(cuda)
         out = br.bitrev_batched(src, b)
@@ -227,7 +227,7 @@ def test_launch_counter_moves(cuda):
 
 
 @pytest.mark.parametrize("E", [4, 8, 16, 2])
-@pytest.mark.parametrize("path", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("path", [0, 1, 2, 3, 4, 5])
 def test_guard_bands_untouched(cuda, E, path):
     """Out-of-bounds writes check (compute-sanitizer is closed on this pool):
     every staging path runs on a batched slice that sits inside a buffer with
@@ -244,7 +244,7 @@ def test_guard_bands_untouched(cuda, E, path):
     old = (br.get_tile_path(E, inplace), br.get_tile_path(E, False))
     try:
         if E in (4, 8, 16):
-            br.set_tile_path(E, inplace, path if path != 4 or inplace else 0)
+            br.set_tile_path(E, inplace, path if path < 4 or inplace else 0)
         if inplace:
             br.bitrev_batched_inplace(rows, b)
             got = rows
