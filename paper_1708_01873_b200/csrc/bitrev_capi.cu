@@ -1045,14 +1045,13 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   // (complex64: QX = 7, 128-element rows, up to 7 stages; complex128: QX = 6,
   // 64-element rows, up to 6 stages).  Rows too big for the small kernel are
   // always wide enough (b >= 13 resp. 12 >= QX + QZ).
-  // QZ (source pieces) per (E, stages), measured (tools/fft_stage_sweep.py,
-  // profiles/r01_fft_qz_ab.txt).  complex128 with 128-byte pieces has 8 rows
-  // per tile, and with 2 rows per warp pass half the warps idle in the
-  // butterfly drain; 256-byte pieces (16 rows) keep all 8 busy: +29 % at 4
-  // stages, +16 % at 6, -2.5 % at 1.  complex64 with 256-byte pieces needs
-  // ~165 registers (1 CTA/SM): it only pays at 7 stages (+2.4 %).
-  const bool wide = E == 8 ? stages == 7 : stages >= 2;
-  const int qx = E == 8 ? 7 : 6, qz = (E == 8 ? 4 : 3) + (wide ? 1 : 0);
+  // QZ = 4 source-piece bits for both types (tools/fft_stage_sweep.py,
+  // profiles/r01_fft_qz_ab.txt): complex128 with QZ = 3 has 8 rows per tile,
+  // and with 2 rows per warp pass half the warps idled in the butterfly drain
+  // (16 rows: +29 % at 4 stages); complex64 with QZ = 5 needs ~170 registers
+  // (1 CTA/SM) and trails QZ = 4 once the drain's shared-memory conflicts are
+  // gone.
+  const int qx = E == 8 ? 7 : 6, qz = 4;
   if (stages > qx || b < qx + qz) return BITREV_ESTAGES;
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
@@ -1069,15 +1068,14 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   }
   if (E == 8) {
     switch (stages) {
-      FFT_LAUNCH(8, 7, 4, 1) FFT_LAUNCH(8, 7, 4, 2)
-      FFT_LAUNCH(8, 7, 4, 3) FFT_LAUNCH(8, 7, 4, 4) FFT_LAUNCH(8, 7, 4, 5)
-      FFT_LAUNCH(8, 7, 4, 6) FFT_LAUNCH(8, 7, 5, 7)
+      FFT_LAUNCH(8, 7, 4, 1) FFT_LAUNCH(8, 7, 4, 2) FFT_LAUNCH(8, 7, 4, 3)
+      FFT_LAUNCH(8, 7, 4, 4) FFT_LAUNCH(8, 7, 4, 5) FFT_LAUNCH(8, 7, 4, 6)
+      FFT_LAUNCH(8, 7, 4, 7)
     }
   } else {
     switch (stages) {
-      FFT_LAUNCH(16, 6, 3, 1) FFT_LAUNCH(16, 6, 4, 2)
-      FFT_LAUNCH(16, 6, 4, 3) FFT_LAUNCH(16, 6, 4, 4) FFT_LAUNCH(16, 6, 4, 5)
-      FFT_LAUNCH(16, 6, 4, 6)
+      FFT_LAUNCH(16, 6, 4, 1) FFT_LAUNCH(16, 6, 4, 2) FFT_LAUNCH(16, 6, 4, 3)
+      FFT_LAUNCH(16, 6, 4, 4) FFT_LAUNCH(16, 6, 4, 5) FFT_LAUNCH(16, 6, 4, 6)
     }
   }
 #undef FFT_LAUNCH

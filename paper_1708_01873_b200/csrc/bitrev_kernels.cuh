@@ -1314,9 +1314,28 @@ __device__ __forceinline__ void bfly(C& top, C& bot, C w) {
   top = cadd(top, t);
 }
 
+// Per-lane twiddles of the radix-4 drain, loaded once per CTA: they depend
+// only on the lane (read per tile from the shared table they cost 2-8-way
+// conflicting LDS.64: words 2^(QX-s) apart share a bank).  W_{2^s}^k =
+// tw[k << (QX - s)] with tw = W_{2^QX}^j, j < 2^(QX-1).
+template <int E, int QX, int stages>
+struct LaneTw {
+  using C = typename Cplx<E>::T;
+  C w3, w40, w41, w5, w60, w61, w70, w71;
+  __device__ __forceinline__ void load(const C* tw, int ll) {
+    auto W = [&](int s, int k) { return tw[k << (QX - s)]; };
+    const int a = ll & 3, b = ll & 15;
+    if constexpr (stages >= 3) w3 = W(3, a);
+    if constexpr (stages >= 4) { w40 = W(4, a); w41 = W(4, a + 4); }
+    if constexpr (stages >= 5) w5 = W(5, b);
+    if constexpr (stages >= 6) { w60 = W(6, b); w61 = W(6, b + 16); }
+    if constexpr (QX >= 7 && stages >= 7) { w70 = W(7, ll); w71 = W(7, ll + 32); }
+  }
+};
+
 template <int E, int QX, int QZ, int stages>
 __device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_t dst_row,
-                                                  const typename Cplx<E>::T* tw, bool inverse) {
+                                                  const LaneTw<E, QX, stages>& lt, bool inverse) {
   using C = typename Cplx<E>::T;
   using T = Rect<E, QX, QZ>;
   constexpr int V = T::V, LPR = (1 << QX) / 4, RPP = 32 / LPR;
@@ -1328,23 +1347,51 @@ __device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_
   const int h = lane / LPR, ll = lane % LPR;
   auto row_of = [&](int i) { return (warp + i * NWARPS) * RPP + h; };
   auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
-  // twiddles: W_{2^s}^k = tw[k << (QX - s)] (tw = W_{2^QX}^j, j < 2^(QX-1))
-  auto W = [&](int s, int k) { return tw[k << (QX - s)]; };
   const C w4 = inverse ? C{0, 1} : C{0, -1};
-  const int a = ll & 3, b = ll & 15;
   C v[NR][4];
+  // Layout A straight from the staged tile: lane ll needs the 4/V chunks
+  // (4 ll)/V + c of its row.  Reading them in lane order would put a quarter
+  // warp on 4 (complex64) or 2 (complex128) of the 8 16-byte bank slots, so
+  // each lane starts at a rotated chunk -- c ^ ((ll >> 2) & 1), resp.
+  // (c + (ll >> 1)) & 3 -- which covers all 8 slots, and selects put the
+  // chunks back in order.
+  auto sel = [](bool p, const uint4& x, const uint4& y) {
+    return make_uint4(p ? x.x : y.x, p ? x.y : y.y, p ? x.z : y.z, p ? x.w : y.w);
+  };
 #pragma unroll
-  for (int i = 0; i < NR; ++i) {  // layout A straight from the staged tile
+  for (int i = 0; i < NR; ++i) {
     const int z = row_of(i);
+    if constexpr (E == 8) {
+      const int c0 = (ll >> 2) & 1;
+      const uint4 q0 = U[sidx(z, 2 * ll + c0)], q1 = U[sidx(z, 2 * ll + (c0 ^ 1))];
+      const uint4 lo = sel(c0, q1, q0), hi = sel(c0, q0, q1);
+      v[i][0] = make_float2(__uint_as_float(lo.x), __uint_as_float(lo.y));
+      v[i][1] = make_float2(__uint_as_float(lo.z), __uint_as_float(lo.w));
+      v[i][2] = make_float2(__uint_as_float(hi.x), __uint_as_float(hi.y));
+      v[i][3] = make_float2(__uint_as_float(hi.z), __uint_as_float(hi.w));
+    } else {
+      const int r = (ll >> 1) & 3;
+      uint4 q[4];
 #pragma unroll
-    for (int c = 0; c < 4 / V; ++c) {
-      const uint4 q = U[sidx(z, (4 * ll) / V + c)];
-      if constexpr (E == 8) {
-        v[i][2 * c] = make_float2(__uint_as_float(q.x), __uint_as_float(q.y));
-        v[i][2 * c + 1] = make_float2(__uint_as_float(q.z), __uint_as_float(q.w));
-      } else {
-        v[i][c] = make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
+      for (int c = 0; c < 4; ++c) q[c] = U[sidx(z, 4 * ll + ((c + r) & 3))];  // chunk (c+r)&3
+      if (r & 1) {  // rotate by one: q[j] <- q[j-1]
+        const uint4 t = q[3];
+        q[3] = q[2];
+        q[2] = q[1];
+        q[1] = q[0];
+        q[0] = t;
       }
+      if (r & 2) {  // rotate by two
+        uint4 t = q[0];
+        q[0] = q[2];
+        q[2] = t;
+        t = q[1];
+        q[1] = q[3];
+        q[3] = t;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        v[i][c] = make_double2(__hiloint2double(q[c].y, q[c].x), __hiloint2double(q[c].w, q[c].z));
     }
   }
   __syncwarp();
@@ -1377,34 +1424,38 @@ __device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_
   // stages 3, 4 (layout B)
   if constexpr (stages >= 3) {
     to_layout(1);
-    const C w3 = W(3, a);
 #pragma unroll
-    for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][1], w3); bfly(v[i][2], v[i][3], w3); }
+    for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][1], lt.w3); bfly(v[i][2], v[i][3], lt.w3); }
     if constexpr (stages >= 4) {
-      const C w40 = W(4, a), w41 = W(4, a + 4);
 #pragma unroll
-      for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][2], w40); bfly(v[i][1], v[i][3], w41); }
+      for (int i = 0; i < NR; ++i) {
+        bfly(v[i][0], v[i][2], lt.w40);
+        bfly(v[i][1], v[i][3], lt.w41);
+      }
     }
   }
   // stages 5, 6 (layout C)
   if constexpr (stages >= 5) {
     to_layout(2);
-    const C w5 = W(5, b);
 #pragma unroll
-    for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][1], w5); bfly(v[i][2], v[i][3], w5); }
+    for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][1], lt.w5); bfly(v[i][2], v[i][3], lt.w5); }
     if constexpr (stages >= 6) {
-      const C w60 = W(6, b), w61 = W(6, b + 16);
 #pragma unroll
-      for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][2], w60); bfly(v[i][1], v[i][3], w61); }
+      for (int i = 0; i < NR; ++i) {
+        bfly(v[i][0], v[i][2], lt.w60);
+        bfly(v[i][1], v[i][3], lt.w61);
+      }
     }
   }
   // stage 7 (layout D, complex64 only)
   if constexpr (QX >= 7) {
     if constexpr (stages >= 7) {
       to_layout(3);
-      const C w70 = W(7, ll), w71 = W(7, ll + 32);
 #pragma unroll
-      for (int i = 0; i < NR; ++i) { bfly(v[i][0], v[i][2], w70); bfly(v[i][1], v[i][3], w71); }
+      for (int i = 0; i < NR; ++i) {
+        bfly(v[i][0], v[i][2], lt.w70);
+        bfly(v[i][1], v[i][3], lt.w71);
+      }
     }
   }
   // store from whatever layout the last stage left: for each m every layout's
@@ -1486,6 +1537,9 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS, STAGES >= 5 ? BITREV
   uint64_t t = blockIdx.x;
   if (t >= a.ntiles) return;
   load(t);
+  __syncthreads();  // publish twq
+  LaneTw<E, QX, STAGES> lt;
+  lt.load(twq, (threadIdx.x & 31) % ((1 << QX) / 4));
   for (;;) {
     const uint64_t bi = t >> a.m, y = t & mmask;
 #pragma unroll
@@ -1500,8 +1554,8 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS, STAGES >= 5 ? BITREV
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) load(tn);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
-    if (BITREV_FFT_RADIX4) {  // twq was published by the staging barrier above
-      fft_rows_drain_r4<E, QX, QZ, STAGES>(smem, dbase, dst_row, twq, fa.inverse != 0);
+    if (BITREV_FFT_RADIX4) {
+      fft_rows_drain_r4<E, QX, QZ, STAGES>(smem, dbase, dst_row, lt, fa.inverse != 0);
     } else {
       fft_rows_drain<E, QX, QZ>(smem, dbase, dst_row, tw, fa.stages, fa.inverse != 0);
     }
