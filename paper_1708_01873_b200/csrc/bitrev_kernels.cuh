@@ -26,12 +26,13 @@
 //
 // Kernel families in this file (selection and measured defaults: bitrev_capi.cu)
 //   bitrev_oop_tile_kernel       out of place, square register tiles (above)
-//   bitrev_oop_rect_kernel       out of place, 2^QX x 2^QZ register tiles: short
-//                                source pieces, 1 KB destination rows
+//   bitrev_oop_rect_kernel       out of place, 2^QX x 2^QZ register tiles: 1 KB
+//                                destination rows, 256-byte source pieces
 //   bitrev_inplace_tile_kernel   in place, tile PAIRS {y, rev y}; work items from
 //                                the compact pair enumeration (pair_from_index)
 //   bitrev_ring_kernel           warp-specialised TMA ring: cp.async.bulk rows or
 //                                one cp.async.bulk.tensor per tile, mbarriers
+//   bitrev_inplace_tstore_kernel in place, register loads + TMA tensor stores
 //   bitrev_inplace_cpa_kernel    in place through element-granular cp.async
 //   bitrev_scatter_tile_kernel   sharded plan: local reversal stored into peers
 //   bitrev_fft_rect_kernel       FFT pre-pass: rect tiles + up to 7 DIT stages
@@ -64,9 +65,6 @@
 #endif
 #ifndef BITREV_FFT_MINB
 #define BITREV_FFT_MINB 1  // min CTAs/SM for the 5..7-stage FFT kernels (register cap)
-#endif
-#ifndef BITREV_FFT_RADIX4
-#define BITREV_FFT_RADIX4 1  // FFT pre-pass drain: radix-4 layout passes (1) or shuffles (0)
 #endif
 #ifndef BITREV_RING_BUDGET_KB
 #define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
@@ -1127,13 +1125,13 @@ __global__ void __launch_bounds__(CpaTile<E, Q>::THREADS)
 // blocks of 2^s with twiddles W_{2^s}^k, k < 2^(s-1).  Stages 1..Q therefore
 // stay inside aligned blocks of 2^Q outputs -- exactly one destination row of
 // a tile -- and their twiddles depend only on the position inside the row.
-// The drain below runs them on the row before storing it: lane l of a warp
-// holds row elements l (and l + 32 for Q = 6), stages 1..5 exchange through
-// __shfl_xor, stage 6 is lane-local.  HBM traffic stays 2*n*E.
+// The drain (fft_rows_drain_r4) runs them on each row before storing it, as
+// in-register radix-4 passes between lane layouts.  HBM traffic stays 2*n*E.
 //
 // Complex element types: E = 8 (complex64, float math) and E = 16
 // (complex128, double math).  Twiddles W_{2^Q}^j = exp(-/+ 2 pi i j / 2^Q)
-// are computed once per CTA in double precision into shared memory.
+// are computed once per CTA in double precision into shared memory; each
+// lane then keeps the few it needs in registers (LaneTw).
 
 template <int E> struct Cplx;
 template <> struct Cplx<8> {
@@ -1153,131 +1151,12 @@ template <typename T>
 __device__ __forceinline__ T cadd(T a, T b) { return {a.x + b.x, a.y + b.y}; }
 template <typename T>
 __device__ __forceinline__ T csub(T a, T b) { return {a.x - b.x, a.y - b.y}; }
-__device__ __forceinline__ float2 shfl_xor_c(float2 v, int m) {
-  return {__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m)};
-}
-__device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
-  return {__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m)};
-}
 
-// Q = 6 drain with all of a warp's rows in flight at once (ILP across rows):
-// 64 destination rows, RPW per warp, two elements per lane and row.
-//   complex64:  lane holds x' = 2l, 2l+1 (one 16-byte chunk): stage 1 is
-//               lane-local, stages 2..6 pair lanes l ^ 2^(s-2);
-//   complex128: lane holds x' = l, l+32: stages 1..5 pair lanes l ^ 2^(s-1),
-//               stage 6 is lane-local.
 struct FftArgs {
   TileArgs t;
   int stages;   // DIT stages fused (<= QX)
   int inverse;  // 1: conjugate twiddles (unnormalised inverse transform)
 };
-
-// FFT on destination rows of 2^QX elements held in a rectangular tile's
-// shared buffer U[z][chunk] (Rect<E, QX, QZ> swizzle).  Lanes hold 4 adjacent
-// elements x' = 4 ll + j; LPR = 2^QX / 4 lanes per row (16 or 32), so a warp
-// transforms 32 / LPR rows per pass.  Stages 1 and 2 are lane-local with
-// trivial twiddles (1, -/+ i); stages 3..QX exchange with lane ll ^ 2^(s-3)
-// inside the row's lane group, one complex multiply per element,
-// branch-free (u + sign * t * w).  Twiddles W_{2^QX}^j come from `tw`.
-// Twiddles of stages 3..QX in shared memory, laid out per stage as
-// T_s[j][l'] = W_{2^s}^{4 l' + j} (l' < 2^(s-3)) at offset 2^(s-1) - 4: a lane
-// with l' = ll mod 2^(s-3) reads word l' of row j, so the lanes of a warp
-// read consecutive words (or broadcast) -- no bank conflicts, no registers.
-__host__ __device__ constexpr int tw_offset(int s) { return (1 << (s - 1)) - 4; }
-
-template <int E, int QX, int QZ>
-__device__ __forceinline__ void fft_rows_drain(const uint4* U, char* dbase, uint64_t dst_row,
-                                               const typename Cplx<E>::T* tw, int stages,
-                                               bool inverse) {
-  using C = typename Cplx<E>::T;
-  using Rl = typename Cplx<E>::R;
-  using T = Rect<E, QX, QZ>;
-  constexpr int V = T::V, LPR = (1 << QX) / 4, RPP = 32 / LPR;  // rows per warp pass
-  constexpr int NWARPS = T::THREADS / 32;
-  constexpr int ROWS = 1 << QZ;
-  // all rows of a warp are transformed together (independent shuffle chains)
-  constexpr int NR = (ROWS + NWARPS * RPP - 1) / (NWARPS * RPP);
-  static_assert(LPR == 16 || LPR == 32, "rows of 64 or 128 elements");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp * RPP >= ROWS) return;  // warp-uniform: more warps than rows
-  const int h = lane / LPR, ll = lane % LPR;
-  auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
-  auto row_of = [&](int i) { return (warp + i * NWARPS) * RPP + h; };
-  C v[NR][4];
-#pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    const int z = row_of(i);
-#pragma unroll
-    for (int c = 0; c < 4 / V; ++c) {
-      const uint4 q = U[sidx(z, (4 * ll) / V + c)];
-      if constexpr (E == 8) {
-        v[i][2 * c] = make_float2(__uint_as_float(q.x), __uint_as_float(q.y));
-        v[i][2 * c + 1] = make_float2(__uint_as_float(q.z), __uint_as_float(q.w));
-      } else {
-        v[i][c] = make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
-      }
-    }
-  }
-  if (stages >= 1) {
-#pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      const C a0 = v[i][0], a1 = v[i][1], a2 = v[i][2], a3 = v[i][3];
-      v[i][0] = cadd(a0, a1);
-      v[i][1] = csub(a0, a1);
-      v[i][2] = cadd(a2, a3);
-      v[i][3] = csub(a2, a3);
-    }
-  }
-  if (stages >= 2) {
-#pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      const C a0 = v[i][0], a1 = v[i][1], a2 = v[i][2], a3 = v[i][3];
-      const C t = inverse ? C{-a3.y, a3.x} : C{a3.y, -a3.x};  // a3 * W_4^1
-      v[i][0] = cadd(a0, a2);
-      v[i][2] = csub(a0, a2);
-      v[i][1] = cadd(a1, t);
-      v[i][3] = csub(a1, t);
-    }
-  }
-#pragma unroll
-  for (int s = 3; s <= QX; ++s) {
-    if (s > stages) break;
-    const int half = 1 << (s - 1);
-    const int mask = 1 << (s - 3);
-    const bool bottom = ll & mask;
-    const Rl sgn = bottom ? Rl(-1) : Rl(1);
-    const int lp = ll & ((half >> 2) - 1);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const C w = tw[tw_offset(s) + j * (half >> 2) + lp];
-#pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        const C p = shfl_xor_c(v[i][j], mask);
-        const C u = bottom ? p : v[i][j];
-        const C m = cmul(bottom ? v[i][j] : p, w);
-        v[i][j] = C{u.x + sgn * m.x, u.y + sgn * m.y};
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    const int z = row_of(i);
-    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - QZ)) * dst_row +
-                 (uint64_t)(4 * ll) * E;
-    if constexpr (E == 8) {
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        st_vec(drow + c * 16,
-               make_uint4(__float_as_uint(v[i][2 * c].x), __float_as_uint(v[i][2 * c].y),
-                          __float_as_uint(v[i][2 * c + 1].x), __float_as_uint(v[i][2 * c + 1].y)));
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        st_vec(drow + c * 16, make_uint4(__double2loint(v[i][c].x), __double2hiint(v[i][c].x),
-                                         __double2loint(v[i][c].y), __double2hiint(v[i][c].y)));
-    }
-  }
-}
 
 // Radix-4 drain: the row's elements move between lane layouts through the
 // warp's own rows of the tile buffer (nobody else reads them after the load),
@@ -1500,20 +1379,11 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS, STAGES >= 5 ? BITREV
   using C = typename Cplx<E>::T;
   using Rl = typename Cplx<E>::R;
   extern __shared__ __align__(16) uint4 smem[];
-  __shared__ C tw[(1 << QX) - 4];
-  __shared__ C twq[1 << (QX - 1)];  // W_{2^QX}^j for the radix-4 drain
+  __shared__ C twq[1 << (QX - 1)];  // W_{2^QX}^j, j < 2^(QX-1)
   const TileArgs& a = fa.t;
   const uint64_t src_row = (uint64_t)E << (a.b - QX);
   const uint64_t dst_row = (uint64_t)E << (a.b - QZ);
   const uint64_t mmask = (1ull << a.m) - 1;
-  for (int e = threadIdx.x; e < (1 << QX) - 4; e += blockDim.x) {
-    int s = 3;
-    while (e >= tw_offset(s + 1)) ++s;  // stage of table entry e
-    const int q = 1 << (s - 3), j = (e - tw_offset(s)) / q, lp = (e - tw_offset(s)) % q;
-    double sn, cs;
-    sincospi((fa.inverse ? 2.0 : -2.0) * (4 * lp + j) / (1 << s), &sn, &cs);
-    tw[e] = C{(Rl)cs, (Rl)sn};
-  }
   for (int j = threadIdx.x; j < (1 << (QX - 1)); j += blockDim.x) {
     double sn, cs;
     sincospi((fa.inverse ? 2.0 : -2.0) * j / (1 << QX), &sn, &cs);
@@ -1554,11 +1424,7 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS, STAGES >= 5 ? BITREV
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) load(tn);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
-    if (BITREV_FFT_RADIX4) {
-      fft_rows_drain_r4<E, QX, QZ, STAGES>(smem, dbase, dst_row, lt, fa.inverse != 0);
-    } else {
-      fft_rows_drain<E, QX, QZ>(smem, dbase, dst_row, tw, fa.stages, fa.inverse != 0);
-    }
+    fft_rows_drain_r4<E, QX, QZ, STAGES>(smem, dbase, dst_row, lt, fa.inverse != 0);
     if (tn >= a.ntiles) break;
     __syncthreads();
     t = tn;
