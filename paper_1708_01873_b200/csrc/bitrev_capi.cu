@@ -35,7 +35,7 @@ int default_q(int E, bool inplace) {
   switch (E) {
     case 4: return inplace ? 6 : 8;   // out of place: rectangular QX = 8 (path 3)
     case 8: return inplace ? 6 : 7;   // out of place: rectangular QX = 7 (path 3)
-    case 16: return inplace ? 5 : 6;
+    case 16: return 6;                // in place: 2-CTA cluster pairs (path 6)
     default: return 0;
   }
 }
@@ -71,7 +71,9 @@ std::atomic<int> g_path_oop[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -
 std::atomic<int> g_path_ip[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 
 int default_path(int E, bool inplace) {
-  if (inplace) return 0;  // register tile pairs (compact pair enumeration)
+  // in place: register tile pairs (compact pair enumeration); complex128 pairs
+  // of 1 KB-row tiles split over 2-CTA clusters (profiles/r01_inplace_cluster_ab.jsonl)
+  if (inplace) return E == 16 ? 6 : 0;
   switch (E) {
     case 4:
     case 8: return 3;     // rectangular register tiles (1 KB destination rows)
@@ -321,6 +323,44 @@ bool encode_tile_map(CUtensorMap* map, const void* base, int b, int E, int q, in
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// In-place tile pairs split over 2-CTA clusters (path 6): compact pairs only.
+template <int E, int Q, int NT>
+int launch_ip_cluster(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
+  using T = Tile<E, Q, NT>;
+  if (2 * Q > b) return BITREV_ETILE;
+  auto kern = bitrev_inplace_cluster_kernel<E, Q, NT>;
+  const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
+  TileArgs a;
+  memset(&a, 0, sizeof a);
+  a.src = static_cast<const char*>(buf);
+  a.dst = static_cast<char*>(buf);
+  a.b = b;
+  a.m = b - 2 * Q;
+  a.src_bstride = bs * E;
+  a.dst_bstride = bs * E;
+  a.order = 2;
+  a.batch = batch;
+  a.npairs = pair_count(a.m);
+  a.ntiles = (uint64_t)batch * a.npairs;
+  uint64_t clusters = (uint64_t)device_sms() * (uint64_t)per_sm / 2;
+  if (clusters > a.ntiles) clusters = a.ntiles;
+  if (clusters < 1) clusters = 1;
+  a.step_b = clusters / a.npairs;
+  a.step_w = clusters % a.npairs;
+  kern<<<(unsigned)(2 * clusters), T::THREADS, T::BYTES, st>>>(a);
+  return finish_launch();
+}
+
+int dispatch_ip_cluster(int E, int q, void* buf, int b, int64_t batch, int64_t bs,
+                        cudaStream_t st) {
+  if (E == 4 && q == 7) return launch_ip_cluster<4, 7, 256>(buf, b, batch, bs, st);
+  if (E == 8 && q == 6) return launch_ip_cluster<8, 6, 256>(buf, b, batch, bs, st);
+  if (E == 8 && q == 7) return launch_ip_cluster<8, 7, 512>(buf, b, batch, bs, st);  // 128 KB tile
+  if (E == 16 && q == 5) return launch_ip_cluster<16, 5, 256>(buf, b, batch, bs, st);
+  if (E == 16 && q == 6) return launch_ip_cluster<16, 6, 256>(buf, b, batch, bs, st);
+  return BITREV_ETILE;
 }
 
 // In-place tile pairs with TMA tensor stores (path 5): compact pairs only.
@@ -614,7 +654,8 @@ int check_common(int b, int E, int64_t batch) {
 // only a few hundred tiles (1.7-3.5 waves), and smaller tiles with more
 // resident CTAs per SM balance it -- up to 1.28x (E=4, b=19, out of place),
 // 1.23x (E=8 in place, b=20), 1.16x (E=16 out of place, b=20), 1.07x (E=8
-// out of place, b=22).  Above the last budget the defaults win.
+// out of place, b=22), 1.2-1.5x (E=16 in place against the cluster default,
+// b = 19..25).  Above the last budget the defaults win.
 struct Tier {
   int q = 0, path = 0;  // q = 0: no tier applies
 };
@@ -639,6 +680,8 @@ Tier mid_tier(int E, bool inplace, uint64_t side_bytes) {
     if (within(64)) t = {4, 0};
   } else if (E == 16 && !inplace) {
     if (within(32)) t = {5, 0};
+  } else if (E == 16 && inplace) {
+    if (within(512)) t = {5, 0};  // single-CTA pairs up to b = 25; clusters from b = 26
   }
   return t;
 }
@@ -750,8 +793,9 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
     return note(dispatch_small(E, a, a, b, batch, batch_stride, batch_stride, st), 0, -1);
   const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
   if (vec_ok && (E == 4 || E == 8 || E == 16)) {
-    const int path = tile_path(E, true);
+    int path = tile_path(E, true);
     const Tier t = mid_tier(E, true, side_bytes(E, b, batch));
+    if (t.q) path = t.path;
     for (int q = clamp_q(t.q ? t.q : current_q(E, true), b); q >= 3; --q) {
       if (path == 4) {
         rc = dispatch_ip_cpa(E, q, a, b, batch, batch_stride, st);
@@ -760,6 +804,10 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
       if (path == 5) {
         rc = dispatch_ip_tstore(E, q, a, b, batch, batch_stride, st);
         if (rc != BITREV_ETILE) return note(rc, q, 5);
+      }
+      if (path == 6) {
+        rc = dispatch_ip_cluster(E, q, a, b, batch, batch_stride, st);
+        if (rc != BITREV_ETILE) return note(rc, q, 6);
       }
       if (path == 1 || path == 2) {
         rc = dispatch_ring(path, E, q, true, a, a, b, batch, batch_stride, batch_stride, st);
@@ -1164,7 +1212,7 @@ int bitrev_get_tile_path(int elem_bytes, int inplace) { return tile_path(elem_by
 
 int bitrev_set_tile_path(int elem_bytes, int inplace, int path) {
   if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16) return BITREV_ETILE;
-  if (path < 0 || path > 5 || (path == 3 && inplace) || (path >= 4 && !inplace))
+  if (path < 0 || path > 6 || (path == 3 && inplace) || (path >= 4 && !inplace))
     return BITREV_ETILE;
   (inplace ? g_path_ip : g_path_oop)[elem_bytes].store(path);
   return BITREV_OK;

@@ -126,7 +126,7 @@ __device__ __forceinline__ void st_vec(void* p, const uint4& v) {
 // ---------------------------------------------------------------------------
 // tile geometry
 
-template <int E, int Q>
+template <int E, int Q, int NT = BITREV_TILE_THREADS>
 struct Tile {
   static constexpr int S = 1 << Q;           // tile side (elements)
   static constexpr int V = 16 / E;           // elements per 16-byte vector
@@ -134,7 +134,7 @@ struct Tile {
   static constexpr int CH = S / V;           // 16-byte chunks per tile row
   static constexpr int ITEMS = CH * CH;      // load items (V loads each)
   static constexpr int WCH = S * CH;         // 16-byte chunks per tile
-  static constexpr int THREADS = ITEMS < BITREV_TILE_THREADS ? ITEMS : BITREV_TILE_THREADS;
+  static constexpr int THREADS = ITEMS < NT ? ITEMS : NT;
   static constexpr int IPT = ITEMS / THREADS;  // load items per thread
   static constexpr int WPT = WCH / THREADS;    // drain chunks per thread
   static constexpr int BYTES = S * S * E;
@@ -151,10 +151,10 @@ __device__ __forceinline__ int swz(int z, int col) {
 }
 
 // Issue the V*IPT loads of one tile (rows at stride row_stride bytes).
-template <int E, int Q, bool STREAM>
-__device__ __forceinline__ void tile_load(uint4 (&r)[Tile<E, Q>::IPT][Tile<E, Q>::V],
+template <int E, int Q, bool STREAM, int NT = BITREV_TILE_THREADS>
+__device__ __forceinline__ void tile_load(uint4 (&r)[Tile<E, Q, NT>::IPT][Tile<E, Q, NT>::V],
                                           const char* tile_base, uint64_t row_stride) {
-  using T = Tile<E, Q>;
+  using T = Tile<E, Q, NT>;
 #pragma unroll
   for (int it = 0; it < T::IPT; ++it) {
     const int id = it * T::THREADS + threadIdx.x;
@@ -202,10 +202,10 @@ __device__ __forceinline__ void stage_col(const uint4 (&a)[16 / E], uint4* U, in
 }
 
 // Register transpose + swizzled STS of one tile into U.
-template <int E, int Q>
-__device__ __forceinline__ void tile_stage(const uint4 (&r)[Tile<E, Q>::IPT][Tile<E, Q>::V],
+template <int E, int Q, int NT = BITREV_TILE_THREADS>
+__device__ __forceinline__ void tile_stage(const uint4 (&r)[Tile<E, Q, NT>::IPT][Tile<E, Q, NT>::V],
                                            uint4* U) {
-  using T = Tile<E, Q>;
+  using T = Tile<E, Q, NT>;
 #pragma unroll
   for (int it = 0; it < T::IPT; ++it) {
     const int id = it * T::THREADS + threadIdx.x;
@@ -217,9 +217,9 @@ __device__ __forceinline__ void tile_stage(const uint4 (&r)[Tile<E, Q>::IPT][Til
 }
 
 // Drain U: row z goes to destination row rev_Q(z) (stride row_stride bytes).
-template <int E, int Q>
+template <int E, int Q, int NT = BITREV_TILE_THREADS>
 __device__ __forceinline__ void tile_drain(const uint4* U, char* dst_base, uint64_t row_stride) {
-  using T = Tile<E, Q>;
+  using T = Tile<E, Q, NT>;
 #pragma unroll
   for (int it = 0; it < T::WPT; ++it) {
     const int id = it * T::THREADS + threadIdx.x;
@@ -250,9 +250,10 @@ struct TileArgs {
 // gridDim.x, without divisions in the loop.
 struct PairCursor {
   uint64_t bi, w;
-  __device__ __forceinline__ void start(const TileArgs& a) {
-    bi = blockIdx.x / a.npairs;
-    w = blockIdx.x - bi * a.npairs;
+  __device__ __forceinline__ void start(const TileArgs& a) { start_at(a, blockIdx.x); }
+  __device__ __forceinline__ void start_at(const TileArgs& a, uint64_t idx) {
+    bi = idx / a.npairs;
+    w = idx - bi * a.npairs;
   }
   __device__ __forceinline__ void next(const TileArgs& a) {
     w += a.step_w;
@@ -599,6 +600,65 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
     char* base = a.dst + bi * a.dst_bstride;
     tile_drain<E, Q>(U0, base + (ry << Q) * E, row_stride);
     if (pair) tile_drain<E, Q>(U1, base + (y << Q) * E, row_stride);
+    if (!more) break;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// in-place tile pairs over a 2-CTA cluster (path 6)
+//
+// The single-CTA pair kernel holds BOTH tiles of a pair in one SM's registers
+// and shared memory, which caps the tile at 512-byte rows: the 1 KB-row shapes
+// (E=16 Q=6, E=8 Q=7) spill or do not fit.  Here the two CTAs of a cluster
+// split the pair: rank 0 loads and stages tile y, rank 1 tile rev(y), each in
+// its own SM.  One cluster barrier (release/acquire) separates "both tiles
+// loaded" from "either region written"; then each CTA drains its tile into
+// the partner's slab.  Both CTAs walk the same pair cursor (one cluster = one
+// work stream), so their barrier counts always match; a palindromic y is
+// handled by rank 0 alone.  No distributed shared memory is touched: the
+// barrier only orders rank 1's loads of region rev(y) before rank 0's stores
+// into it (and vice versa).
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int E, int Q, int NT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+    bitrev_inplace_cluster_kernel(TileArgs a) {
+  using T = Tile<E, Q, NT>;
+  extern __shared__ __align__(16) uint4 smem[];
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
+  const unsigned rank = cluster_rank();
+  uint4 r[T::IPT][T::V];
+  PairCursor pc;
+  pc.start_at(a, blockIdx.x >> 1);
+  if (!pc.valid(a)) return;  // same decision in both CTAs of the cluster
+  auto issue = [&]() {
+    const uint64_t y = pair_from_index(pc.w, a.m), ry = dev_rev(y, a.m);
+    if (rank && ry == y) return;  // palindrome: rank 0 alone
+    tile_load<E, Q, BITREV_IP_NC, NT>(r, a.src + pc.bi * a.src_bstride + ((rank ? ry : y) << Q) * E,
+                                      row_stride);
+  };
+  issue();
+  for (;;) {
+    const uint64_t bi = pc.bi, y = pair_from_index(pc.w, a.m), ry = dev_rev(y, a.m);
+    const bool active = !(rank && ry == y);
+    if (active) tile_stage<E, Q, NT>(r, smem);
+    cluster_sync();  // both tiles of the pair are loaded: either region may now be written
+    pc.next(a);
+    const bool more = pc.valid(a);
+    if (more) issue();
+    if (active)
+      tile_drain<E, Q, NT>(smem, a.dst + bi * a.dst_bstride + ((rank ? y : ry) << Q) * E,
+                           row_stride);
     if (!more) break;
     __syncthreads();
   }

@@ -59,7 +59,7 @@ def test_error_codes_without_gpu():
 
 
 def test_tile_bits_registry():
-    for E, q_oop, q_ip in ((4, 8, 6), (8, 7, 6), (16, 6, 5)):
+    for E, q_oop, q_ip in ((4, 8, 6), (8, 7, 6), (16, 6, 6)):
         assert _lib.get_tile_bits(E, False) == q_oop
         assert _lib.get_tile_bits(E, True) == q_ip
     _lib.set_tile_bits(8, True, 4)
@@ -69,7 +69,7 @@ def test_tile_bits_registry():
     assert _lib.get_tile_order(True) == 2 and _lib.get_tile_order(False) == 0
     for E in (4, 8, 16):
         for ip in (False, True):
-            assert _lib.get_tile_path(E, ip) in (0, 1, 2, 3)
+            assert _lib.get_tile_path(E, ip) in (0, 1, 2, 3, 4, 5, 6)
     with pytest.raises(_lib.BitrevError):
         _lib.set_tile_bits(8, False, 9)
     with pytest.raises(_lib.BitrevError):

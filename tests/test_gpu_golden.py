@@ -155,6 +155,20 @@ def test_complex128_large_sampled_vs_cpu_oracle(cuda, b):
     assert torch.equal(out.view(torch.int64), x.view(torch.int64))
 
 
+@pytest.mark.parametrize("b,batch", [(26, 1), (26, 2), (27, 1)])
+def test_complex128_inplace_cluster_default(cuda, b, batch):
+    """complex128 in place above the mid-size tier runs the 2-CTA cluster pair
+    kernel by default (even and odd middle widths, batched rows); every byte
+    is compared with the device oracle."""
+    x = torch.empty(batch * (1 << b) * 16, dtype=torch.uint8, device=cuda).random_(0, 256)
+    x = x.view(torch.complex128).view(batch, 1 << b)
+    expect = torch.stack([br.oracle_permute(r, b) for r in x])
+    br.bitrev_batched_inplace(x, b)
+    torch.cuda.synchronize()
+    assert br.last_tile() == (6, 6)
+    assert torch.equal(x.view(torch.uint8), expect.view(torch.uint8))
+
+
 @pytest.mark.parametrize("b,G,dtype,chunks", [(12, 2, torch.int64, 1), (16, 4, torch.complex64, 1),
                                               (20, 8, torch.float32, 4), (21, 8, torch.complex128, 2),
                                               (26, 8, torch.complex64, 8), (14, 2, torch.int32, 16)])

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 NP = {4: np.int32, 8: np.int64, 16: np.complex128}
 # (E, inplace) -> default (q, path) above every budget
 LARGE = {(4, False): (8, 3), (4, True): (6, 0), (8, False): (7, 3), (8, True): (6, 0),
-         (16, False): (6, 0), (16, True): (5, 0)}
+         (16, False): (6, 0), (16, True): (6, 6)}
 # (E, inplace, b, expected (q, path)) at each budget and one width above it
 CASES = [
     (4, False, 23, (5, 0)), (4, False, 24, (7, 3)),    # 32 MiB tier: square Q5
@@ -27,7 +27,7 @@ CASES = [
     (8, False, 22, (4, 0)), (8, False, 23, (7, 3)),
     (8, True, 23, (4, 0)), (8, True, 24, (6, 0)),
     (16, False, 21, (5, 0)), (16, False, 22, (6, 0)),
-    (16, True, 22, (5, 0)), (16, True, 23, (5, 0)),    # no tier (default Q5)
+    (16, True, 25, (5, 0)), (16, True, 26, (6, 6)),    # 512 MiB tier: single-CTA pairs
 ]
 # pinned values that differ from the default and from any tier's q
 PIN = {(4, False): 6, (4, True): 7, (8, False): 6, (8, True): 5, (16, False): 4, (16, True): 4}

@@ -77,7 +77,7 @@ def test_every_tile_size(cuda, E, b):
     try:
         for q in qs:
             for order in (0, 1, 2):
-                for path in (0, 1, 2, 4, 5):
+                for path in (0, 1, 2, 4, 5, 6):
                     for inplace in (False, True):
                         br.set_tile_bits(E, inplace, q)
                         br.set_tile_order(inplace, order)
@@ -116,8 +116,35 @@ def test_rect_out_of_place_tiles(cuda, E, q, b, batch):
         br.set_tile_path(E, False, old[1])
 
 
+@pytest.mark.parametrize("E,q", [(4, 7), (8, 6), (8, 7), (16, 5), (16, 6)])
+@pytest.mark.parametrize("b,batch", [(14, 3), (15, 2), (17, 1), (20, 2), (23, 1)])
+def test_cluster_pair_tiles(cuda, E, q, b, batch):
+    """In-place tile pairs split over 2-CTA clusters (path 6), including the
+    1 KB-row shapes the single-CTA kernel cannot hold (E=8 Q=7, E=16 Q=6),
+    palindromic middles (odd and even m) and batched rows."""
+    if 2 * q > b:
+        pytest.skip("tile wider than the array")
+    if (E, q) == (16, 6):
+        pytest.skip("the default shape: below 512 MiB the size tiers route it to Q5; "
+                    "covered at b = 26/27 by test_complex128_inplace_cluster_default")
+    host = rand_bits(1 << b, E, seed=8000 * E + 10 * b + q, batch=batch)
+    expected = orc.oracle_permute(host, b)
+    old = (br.get_tile_bits(E, True), br.get_tile_path(E, True))
+    try:
+        br.set_tile_bits(E, True, q)
+        br.set_tile_path(E, True, 6)
+        a = torch.from_numpy(host).to(cuda)
+        br.bitrev_batched_inplace(a, b)
+        torch.cuda.synchronize()
+        assert br.last_tile() == (q, 6)
+        assert_same(a, expected)
+    finally:
+        br.set_tile_bits(E, True, old[0])
+        br.set_tile_path(E, True, old[1])
+
+
 @pytest.mark.parametrize("order", [0, 2])
-@pytest.mark.parametrize("path", [0, 1, 2, 4, 5])
+@pytest.mark.parametrize("path", [0, 1, 2, 4, 5, 6])
 @pytest.mark.parametrize("E", [4, 8, 16])
 @pytest.mark.parametrize("b,batch", [(12, 2), (13, 3), (14, 3), (15, 5), (19, 2), (22, 1)])
 def test_both_staging_paths(cuda, order, path, E, b, batch):
@@ -227,7 +254,7 @@ def test_launch_counter_moves(cuda):
 
 
 @pytest.mark.parametrize("E", [4, 8, 16, 2])
-@pytest.mark.parametrize("path", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("path", [0, 1, 2, 3, 4, 5, 6])
 def test_guard_bands_untouched(cuda, E, path):
     """Out-of-bounds writes check (compute-sanitizer is closed on this pool):
     every staging path runs on a batched slice that sits inside a buffer with

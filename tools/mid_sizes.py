@@ -68,6 +68,8 @@ def main():
                     cands += [(7, 3), (6, 3)]
                 if E == 4 and not inplace:
                     cands += [(8, 3), (7, 3)]
+                if E == 16 and inplace:
+                    cands += [(6, 6), (5, 6)]
                 for q, p in cands:
                     if 2 * q > b:
                         continue

@@ -19,7 +19,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1708_01873_b200 as br  # noqa: E402
 from paper_1708_01873_b200 import _core  # noqa: E402
 
-QS = {4: [5, 6, 7], 8: [4, 5, 6], 16: [3, 4, 5, 6]}
+QS = {4: [5, 6, 7], 8: [4, 5, 6, 7], 16: [3, 4, 5, 6]}
 DT = {4: torch.float32, 8: torch.float64, 16: torch.complex128}
 
 
