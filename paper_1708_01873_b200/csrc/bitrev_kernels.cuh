@@ -612,8 +612,8 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
 // and shared memory, which caps the tile at 512-byte rows: the 1 KB-row shapes
 // (E=16 Q=6, E=8 Q=7) spill or do not fit.  Here the two CTAs of a cluster
 // split the pair: rank 0 loads and stages tile y, rank 1 tile rev(y), each in
-// its own SM.  One cluster barrier (release/acquire) separates "both tiles
-// loaded" from "either region written"; then each CTA drains its tile into
+// its own SM.  One cluster barrier separates "both tiles loaded" from
+// "either region written"; then each CTA drains its tile into
 // the partner's slab.  Both CTAs walk the same pair cursor (one cluster = one
 // work stream), so their barrier counts always match; a palindromic y is
 // handled by rank 0 alone.  No distributed shared memory is touched: the
@@ -625,9 +625,17 @@ __device__ __forceinline__ unsigned cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n"
-               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+// Execution-only cluster barrier.  Across the pair it guards a write-after-
+// read: a CTA arrives only after its loads of the partner's region have
+// returned (their values were consumed by the STS of tile_stage), so no later
+// store can change them, and no CTA ever reads a region another CTA wrote.
+// It gives NO memory ordering, so the CTA's own STS -> LDS hand-off needs the
+// __syncthreads() before it.  A release arrive would make every thread wait
+// for its previous drain's global stores to be performed (ncu: 16 % membar
+// stalls).
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n"
+               "barrier.cluster.wait.aligned;" ::: "memory");
 }
 
 template <int E, int Q, int NT>
@@ -652,7 +660,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     const uint64_t bi = pc.bi, y = pair_from_index(pc.w, a.m), ry = dev_rev(y, a.m);
     const bool active = !(rank && ry == y);
     if (active) tile_stage<E, Q, NT>(r, smem);
-    cluster_sync();  // both tiles of the pair are loaded: either region may now be written
+    __syncthreads();          // this CTA's staged tile is visible to all its threads
+    cluster_sync_relaxed();   // both tiles of the pair are loaded: either region may be written
     pc.next(a);
     const bool more = pc.valid(a);
     if (more) issue();
