@@ -344,7 +344,28 @@ int launch_ip_cluster(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t 
   a.batch = batch;
   a.npairs = pair_count(a.m);
   a.ntiles = (uint64_t)batch * a.npairs;
+  // co-resident clusters: both CTAs of a cluster sit in one GPC, so a GPC with
+  // an odd number of free SMs strands one; a persistent grid larger than this
+  // would run its last clusters as a second wave
   uint64_t clusters = (uint64_t)device_sms() * (uint64_t)per_sm / 2;
+  {
+    static std::atomic<int> cached[kMaxDevices];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int c = (dev >= 0 && dev < kMaxDevices) ? cached[dev].load() : 0;
+    if (c == 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(2 * clusters));
+      cfg.blockDim = dim3(T::THREADS);
+      cfg.dynamicSmemBytes = T::BYTES;
+      if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c <= 0) {
+        cudaGetLastError();
+        c = (int)clusters;
+      }
+      if (dev >= 0 && dev < kMaxDevices) cached[dev].store(c);
+    }
+    if ((uint64_t)c < clusters) clusters = (uint64_t)c;
+  }
   if (clusters > a.ntiles) clusters = a.ntiles;
   if (clusters < 1) clusters = 1;
   a.step_b = clusters / a.npairs;
