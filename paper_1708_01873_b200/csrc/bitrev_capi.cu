@@ -207,11 +207,11 @@ int prepare_kernel(K kernel, int threads, int smem_bytes) {
 // ---------------------------------------------------------------------------
 // tile launches
 
-template <int E, int Q>
+template <int E, int Q, int NT = BITREV_TILE_THREADS>
 int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
                     cudaStream_t st) {
-  using T = Tile<E, Q>;
-  auto kern = bitrev_oop_tile_kernel<E, Q>;
+  using T = Tile<E, Q, NT>;
+  auto kern = bitrev_oop_tile_kernel<E, Q, NT>;
   const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
   TileArgs a;
   a.src = static_cast<const char*>(src);
@@ -546,6 +546,7 @@ int dispatch_oop_tile(int E, int q, const void* src, void* dst, int b, int64_t b
         case 4: return launch_oop_tile<8, 4>(src, dst, b, batch, sbs, dbs, st);
         case 5: return launch_oop_tile<8, 5>(src, dst, b, batch, sbs, dbs, st);
         case 6: return launch_oop_tile<8, 6>(src, dst, b, batch, sbs, dbs, st);
+        case 7: return launch_oop_tile<8, 7, 512>(src, dst, b, batch, sbs, dbs, st);  // 128 KB
       }
       break;
     case 16:

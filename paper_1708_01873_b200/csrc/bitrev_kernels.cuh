@@ -345,10 +345,10 @@ __device__ __forceinline__ uint64_t pair_from_index(uint64_t w, int m) {
 // ---------------------------------------------------------------------------
 // out-of-place tile kernel (replaces _cobra_copy, src/permutations.py:225-249)
 
-template <int E, int Q>
-__global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_OOP)
+template <int E, int Q, int NT = BITREV_TILE_THREADS>
+__global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, BITREV_MINB_OOP)
     bitrev_oop_tile_kernel(TileArgs a) {
-  using T = Tile<E, Q>;
+  using T = Tile<E, Q, NT>;
   extern __shared__ __align__(16) uint4 smem[];
   const uint64_t row_stride = ((uint64_t)E << (a.b - Q)) + BITREV_EXPERIMENT_ROWPAD;
   const uint64_t mmask = (1ull << a.m) - 1;
@@ -360,15 +360,15 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_OOP)
     const uint64_t bi = tt >> a.m, y = work_to_y(tt & mmask, a.m, a.order);
     return a.src + bi * a.src_bstride + (y << Q) * E;
   };
-  tile_load<E, Q, true>(r, src_tile(t), row_stride);
+  tile_load<E, Q, true, NT>(r, src_tile(t), row_stride);
   for (;;) {
     const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
-    tile_stage<E, Q>(r, smem);
+    tile_stage<E, Q, NT>(r, smem);
     __syncthreads();
     const uint64_t tn = t + gridDim.x;
-    if (tn < a.ntiles) tile_load<E, Q, true>(r, src_tile(tn), row_stride);
+    if (tn < a.ntiles) tile_load<E, Q, true, NT>(r, src_tile(tn), row_stride);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << Q) * E;
-    tile_drain<E, Q>(smem, dbase, row_stride);
+    tile_drain<E, Q, NT>(smem, dbase, row_stride);
     if (tn >= a.ntiles) break;
     __syncthreads();
     t = tn;
