@@ -326,11 +326,11 @@ bool encode_tile_map(CUtensorMap* map, const void* base, int b, int E, int q, in
 }
 
 // In-place tile pairs split over 2-CTA clusters (path 6): compact pairs only.
-template <int E, int Q, int NT>
+template <int E, int Q, int NT, int MINB = 1>
 int launch_ip_cluster(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
   using T = Tile<E, Q, NT>;
   if (2 * Q > b) return BITREV_ETILE;
-  auto kern = bitrev_inplace_cluster_kernel<E, Q, NT>;
+  auto kern = bitrev_inplace_cluster_kernel<E, Q, NT, MINB>;
   const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
   TileArgs a;
   memset(&a, 0, sizeof a);
@@ -377,7 +377,7 @@ int launch_ip_cluster(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t 
 int dispatch_ip_cluster(int E, int q, void* buf, int b, int64_t batch, int64_t bs,
                         cudaStream_t st) {
   if (E == 4 && q == 7) return launch_ip_cluster<4, 7, 256>(buf, b, batch, bs, st);
-  if (E == 8 && q == 6) return launch_ip_cluster<8, 6, 256>(buf, b, batch, bs, st);
+  if (E == 8 && q == 6) return launch_ip_cluster<8, 6, 256, 2>(buf, b, batch, bs, st);  // 2 CTAs/SM
   if (E == 8 && q == 7) return launch_ip_cluster<8, 7, 512>(buf, b, batch, bs, st);  // 128 KB tile
   if (E == 16 && q == 5) return launch_ip_cluster<16, 5, 256>(buf, b, batch, bs, st);
   if (E == 16 && q == 6) return launch_ip_cluster<16, 6, 256>(buf, b, batch, bs, st);

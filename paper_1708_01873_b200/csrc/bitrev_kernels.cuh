@@ -638,8 +638,8 @@ __device__ __forceinline__ void cluster_sync_relaxed() {
                "barrier.cluster.wait.aligned;" ::: "memory");
 }
 
-template <int E, int Q, int NT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+template <int E, int Q, int NT, int MINB = 1>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, MINB)
     bitrev_inplace_cluster_kernel(TileArgs a) {
   using T = Tile<E, Q, NT>;
   extern __shared__ __align__(16) uint4 smem[];

@@ -22,5 +22,9 @@ for spec in "cfg2:bitrev_" "cfg3-16:bitrev_" "cfg3-4:bitrev_" "cfg3-8:bitrev_" "
   python bench.py --workload $w $P > $O/plain_$w.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
         -o $O/prof_$w python bench.py --workload $w $P > $O/ncu_$w.log 2>&1
+  # gpurun copies back <= 64 MiB: keep the raw page of every capture, and the
+  # full report of the headline kernel only
+  ncu -i $O/prof_$w.ncu-rep --page raw --csv > $O/prof_${w}_raw.csv 2>/dev/null
+  [ "$w" = cfg2 ] || rm -f $O/prof_$w.ncu-rep
 done
 echo gpu_round done

@@ -16,10 +16,22 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 TIME = {"ns": 1e-3, "us": 1, "ms": 1e3}
 
 traffic = {}
-for rep in sorted(OUT.glob("prof_*.ncu-rep")):
-    w = rep.stem[len("prof_"):]
-    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"],
-                         capture_output=True, text=True).stdout
+def raw_pages():
+    """(workload, raw-page CSV text): exported on the box (prof_<w>_raw.csv),
+    else read from a full report (prof_<w>.ncu-rep)."""
+    seen = set()
+    for csvf in sorted(OUT.glob("prof_*_raw.csv")):
+        w = csvf.name[len("prof_"):-len("_raw.csv")]
+        seen.add(w)
+        yield w, csvf.read_text()
+    for rep in sorted(OUT.glob("prof_*.ncu-rep")):
+        w = rep.stem[len("prof_"):]
+        if w not in seen:
+            yield w, subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"],
+                                    capture_output=True, text=True).stdout
+
+
+for w, raw in raw_pages():
     rows = list(csv.reader(io.StringIO(raw)))
     if len(rows) < 3:
         continue
