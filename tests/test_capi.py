@@ -76,6 +76,25 @@ def test_tile_bits_registry():
         _lib.set_tile_bits(2, False, 5)
 
 
+def test_tile_path_registry_and_last_tile():
+    """Staging paths: 3 is out-of-place only, 4/5/6 in-place only; defaults
+    are the measured ones; bitrev_last_tile rejects NULL outputs."""
+    assert [_lib.get_tile_path(E, False) for E in (4, 8, 16)] == [3, 3, 0]
+    assert [_lib.get_tile_path(E, True) for E in (4, 8, 16)] == [0, 0, 6]
+    for E, ip, path in ((8, True, 3), (8, False, 4), (8, False, 5), (8, False, 6),
+                        (8, True, 7), (8, True, -1), (2, True, 0)):
+        with pytest.raises(_lib.BitrevError):
+            _lib.set_tile_path(E, ip, path)
+    for path in (4, 5, 6, 0):
+        _lib.set_tile_path(16, True, path)
+        assert _lib.get_tile_path(16, True) == path
+    _lib.set_tile_path(16, True, 6)
+    lib = _lib.load()
+    assert lib.bitrev_last_tile(None, None) == -3
+    if _lib.launch_count() == 0:  # nothing launched in this process yet: zeros
+        assert _lib.last_tile() == (0, 0)
+
+
 def test_tile_order_registry():
     old = _lib.get_tile_order(True)
     _lib.set_tile_order(True, 1)
