@@ -964,21 +964,19 @@ int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int
     PIPE_TRY(cudaEventRecord(ev_out[s], sout));
   }
   if (own) {
-    // the allocation's last users are on sout
-    PIPE_TRY(cudaStreamWaitEvent(sin, ev_out[(count - 1) % kSlots], 0));
+    // every use of the slots is ordered before the last D2H on sout (each
+    // kernel waits for its H2D, each D2H for its kernel)
     PIPE_TRY(cudaFreeAsync(own, sout));
     own = nullptr;
   }
   PIPE_TRY(cudaStreamSynchronize(sout));
 done:
 #undef PIPE_TRY
-  if (own) {
-    cudaStreamSynchronize(sin);
-    cudaFree(own);
-  }
+  // error or not, nothing may still be using the slots or the events below
   if (sin) cudaStreamSynchronize(sin);
   if (sk) cudaStreamSynchronize(sk);
   if (sout) cudaStreamSynchronize(sout);
+  if (own) cudaFree(own);  // only on an error path: the normal path frees stream-ordered
   for (int i = 0; i < kSlots; ++i) {
     if (ev_in[i]) cudaEventDestroy(ev_in[i]);
     if (ev_k[i]) cudaEventDestroy(ev_k[i]);
