@@ -138,6 +138,13 @@ int grid_for(uint64_t work, int per_sm, int threads_hint = 0) {
   return (int)(g > 0 ? g : 1);
 }
 
+// Streaming (evict-first) stores for launches whose working set is far beyond
+// the 126 MB L2 (>= 64 MiB per side); the default large-array shapes have a
+// CS = true kernel instantiation for it (bitrev_kernels.cuh, st_vec).
+bool stream_stores(int E, int b, int64_t batch) {
+  return ((uint64_t)E << b) * (uint64_t)batch >= (64ull << 20);
+}
+
 // In-place work items: tile order 2 = compact pair enumeration
 // (pair_from_index: one item per unordered pair, walked with a division-free
 // cursor); other orders visit every y and skip items with rev(y) < y.
@@ -211,7 +218,9 @@ template <int E, int Q, int NT = BITREV_TILE_THREADS>
 int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
                     cudaStream_t st) {
   using T = Tile<E, Q, NT>;
-  auto kern = bitrev_oop_tile_kernel<E, Q, NT>;
+  auto kern = bitrev_oop_tile_kernel<E, Q, NT, false>;
+  if constexpr (E == 16 && Q == 6 && NT == BITREV_TILE_THREADS)
+    if (stream_stores(E, b, batch)) kern = bitrev_oop_tile_kernel<E, Q, NT, true>;
   const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
   TileArgs a;
   a.src = static_cast<const char*>(src);
@@ -232,7 +241,9 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
 template <int E, int Q, bool COMPACT>
 int launch_ip_tile_mode(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
   using T = Tile<E, Q>;
-  auto kern = bitrev_inplace_tile_kernel<E, Q, COMPACT>;
+  auto kern = bitrev_inplace_tile_kernel<E, Q, COMPACT, false>;
+  if constexpr (COMPACT && Q == 6 && (E == 4 || E == 8))
+    if (stream_stores(E, b, batch)) kern = bitrev_inplace_tile_kernel<E, Q, COMPACT, true>;
   const int per_sm = prepare_kernel(kern, T::THREADS, 2 * T::BYTES);
   TileArgs a;
   a.src = static_cast<const char*>(buf);
@@ -330,7 +341,9 @@ template <int E, int Q, int NT, int MINB = 1>
 int launch_ip_cluster(void* buf, int b, int64_t batch, int64_t bs, cudaStream_t st) {
   using T = Tile<E, Q, NT>;
   if (2 * Q > b) return BITREV_ETILE;
-  auto kern = bitrev_inplace_cluster_kernel<E, Q, NT, MINB>;
+  auto kern = bitrev_inplace_cluster_kernel<E, Q, NT, MINB, false>;
+  if constexpr (E == 16 && Q == 6)
+    if (stream_stores(E, b, batch)) kern = bitrev_inplace_cluster_kernel<E, Q, NT, MINB, true>;
   const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
   TileArgs a;
   memset(&a, 0, sizeof a);
@@ -483,7 +496,9 @@ int launch_oop_rect(const void* src, void* dst, int b, int64_t batch, int64_t sb
                     cudaStream_t st) {
   using T = Rect<E, QX, QZ>;
   if (b < QX + QZ) return BITREV_ETILE;
-  auto kern = bitrev_oop_rect_kernel<E, QX, QZ>;
+  auto kern = bitrev_oop_rect_kernel<E, QX, QZ, false>;
+  if constexpr ((E == 4 && QX == 8 && QZ == 6) || (E == 8 && QX == 7 && QZ == 5))
+    if (stream_stores(E, b, batch)) kern = bitrev_oop_rect_kernel<E, QX, QZ, true>;
   const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
   TileArgs a;
   a.src = static_cast<const char*>(src);

@@ -101,8 +101,14 @@ template <> struct Word<8> { using T = unsigned long long; };
 template <> struct Word<16> { using T = uint4; };
 
 // 128-bit global accesses.  Source rows are read exactly once per launch, so the
-// loads bypass L1 allocation; stores are plain (the permuted array is normally
-// consumed next, e.g. by the first FFT butterfly stage, so keep it in L2).
+// loads bypass L1 allocation.  Stores are plain by default (the permuted array
+// is normally consumed next, e.g. by the first FFT butterfly stage, so keep it
+// in L2).  The default large-array shapes also have a CS = true instantiation
+// with streaming (evict-first) stores, which the host selects for launches of
+// >= 64 MiB per side: at b = 30 out of place +1-3 % (profiles/
+// r01_streaming_stores_ab.txt); for L2-sized arrays streaming stores cost
+// ~1.5 %.  A runtime flag instead of a template parameter perturbed register
+// allocation (E=4 rect tiles fell to 128 registers and 2 CTAs/SM).
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -117,10 +123,16 @@ __device__ __forceinline__ uint4 ld_plain(const void* p) {
                : "l"(p));
   return r;
 }
+template <bool CS = false>
 __device__ __forceinline__ void st_vec(void* p, const uint4& v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
+  if constexpr (CS)
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+  else
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -217,7 +229,7 @@ __device__ __forceinline__ void tile_stage(const uint4 (&r)[Tile<E, Q, NT>::IPT]
 }
 
 // Drain U: row z goes to destination row rev_Q(z) (stride row_stride bytes).
-template <int E, int Q, int NT = BITREV_TILE_THREADS>
+template <int E, int Q, int NT = BITREV_TILE_THREADS, bool CS = false>
 __device__ __forceinline__ void tile_drain(const uint4* U, char* dst_base, uint64_t row_stride) {
   using T = Tile<E, Q, NT>;
 #pragma unroll
@@ -227,7 +239,7 @@ __device__ __forceinline__ void tile_drain(const uint4* U, char* dst_base, uint6
     const int z = id / T::CH;
     const uint4 v = U[swz<E, Q>(z, col)];
     const uint64_t rz = __brev((unsigned)z) >> (32 - Q);
-    st_vec(dst_base + rz * row_stride + (uint64_t)col * 16, v);
+    st_vec<CS>(dst_base + rz * row_stride + (uint64_t)col * 16, v);
   }
 }
 
@@ -345,7 +357,7 @@ __device__ __forceinline__ uint64_t pair_from_index(uint64_t w, int m) {
 // ---------------------------------------------------------------------------
 // out-of-place tile kernel (replaces _cobra_copy, src/permutations.py:225-249)
 
-template <int E, int Q, int NT = BITREV_TILE_THREADS>
+template <int E, int Q, int NT = BITREV_TILE_THREADS, bool CS = false>
 __global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, BITREV_MINB_OOP)
     bitrev_oop_tile_kernel(TileArgs a) {
   using T = Tile<E, Q, NT>;
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, BITREV_MINB_OOP)
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) tile_load<E, Q, true, NT>(r, src_tile(tn), row_stride);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << Q) * E;
-    tile_drain<E, Q, NT>(smem, dbase, row_stride);
+    tile_drain<E, Q, NT, CS>(smem, dbase, row_stride);
     if (tn >= a.ntiles) break;
     __syncthreads();
     t = tn;
@@ -405,7 +417,7 @@ struct Rect {
   static_assert(ITEMS % THREADS == 0 && WCH % THREADS == 0, "even split");
 };
 
-template <int E, int QX, int QZ>
+template <int E, int QX, int QZ, bool CS = false>
 __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
     bitrev_oop_rect_kernel(TileArgs a) {
   using T = Rect<E, QX, QZ>;
@@ -456,7 +468,7 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
       const int id = it * T::THREADS + threadIdx.x;
       const int col = id % T::GX, z = id / T::GX;
       const uint64_t rz = __brev((unsigned)z) >> (32 - QZ);
-      st_vec(dbase + rz * dst_row + (uint64_t)col * 16, smem[sidx(z, col)]);
+      st_vec<CS>(dbase + rz * dst_row + (uint64_t)col * 16, smem[sidx(z, col)]);
     }
     if (tn >= a.ntiles) break;
     __syncthreads();
@@ -533,7 +545,7 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS)
 // two CTAs ever touch the same element and both tiles are resident before the
 // first write.
 
-template <int E, int Q, bool COMPACT>
+template <int E, int Q, bool COMPACT, bool CS = false>
 __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
     bitrev_inplace_tile_kernel(TileArgs a) {
   using T = Tile<E, Q>;
@@ -598,8 +610,8 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
     const bool more = cur_valid();
     if (more) issue();
     char* base = a.dst + bi * a.dst_bstride;
-    tile_drain<E, Q>(U0, base + (ry << Q) * E, row_stride);
-    if (pair) tile_drain<E, Q>(U1, base + (y << Q) * E, row_stride);
+    tile_drain<E, Q, BITREV_TILE_THREADS, CS>(U0, base + (ry << Q) * E, row_stride);
+    if (pair) tile_drain<E, Q, BITREV_TILE_THREADS, CS>(U1, base + (y << Q) * E, row_stride);
     if (!more) break;
     __syncthreads();
   }
@@ -638,7 +650,7 @@ __device__ __forceinline__ void cluster_sync_relaxed() {
                "barrier.cluster.wait.aligned;" ::: "memory");
 }
 
-template <int E, int Q, int NT, int MINB = 1>
+template <int E, int Q, int NT, int MINB = 1, bool CS = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, MINB)
     bitrev_inplace_cluster_kernel(TileArgs a) {
   using T = Tile<E, Q, NT>;
@@ -666,8 +678,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, MINB)
     const bool more = pc.valid(a);
     if (more) issue();
     if (active)
-      tile_drain<E, Q, NT>(smem, a.dst + bi * a.dst_bstride + ((rank ? y : ry) << Q) * E,
-                           row_stride);
+      tile_drain<E, Q, NT, CS>(smem, a.dst + bi * a.dst_bstride + ((rank ? y : ry) << Q) * E,
+                               row_stride);
     if (!more) break;
     __syncthreads();
   }
