@@ -123,6 +123,16 @@ __device__ __forceinline__ uint4 ld_plain(const void* p) {
                : "l"(p));
   return r;
 }
+#ifndef BITREV_LD_CS
+#define BITREV_LD_CS 0  // streaming instantiations also load with .cs (evict-first)
+#endif
+__device__ __forceinline__ uint4 ld_cs(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
 template <bool CS = false>
 __device__ __forceinline__ void st_vec(void* p, const uint4& v) {
   if constexpr (CS)
@@ -163,7 +173,7 @@ __device__ __forceinline__ int swz(int z, int col) {
 }
 
 // Issue the V*IPT loads of one tile (rows at stride row_stride bytes).
-template <int E, int Q, bool STREAM, int NT = BITREV_TILE_THREADS>
+template <int E, int Q, bool STREAM, int NT = BITREV_TILE_THREADS, bool LCS = false>
 __device__ __forceinline__ void tile_load(uint4 (&r)[Tile<E, Q, NT>::IPT][Tile<E, Q, NT>::V],
                                           const char* tile_base, uint64_t row_stride) {
   using T = Tile<E, Q, NT>;
@@ -175,7 +185,8 @@ __device__ __forceinline__ void tile_load(uint4 (&r)[Tile<E, Q, NT>::IPT][Tile<E
 #pragma unroll
     for (int k = 0; k < T::V; ++k) {
       const char* p = tile_base + (uint64_t)(g + k * T::CH) * row_stride + (uint64_t)c * 16;
-      r[it][k] = STREAM ? ld_stream(p) : ld_plain(p);
+      if constexpr (LCS) r[it][k] = ld_cs(p);
+      else r[it][k] = STREAM ? ld_stream(p) : ld_plain(p);
     }
   }
 }
@@ -372,13 +383,13 @@ __global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, BITREV_MINB_OOP)
     const uint64_t bi = tt >> a.m, y = work_to_y(tt & mmask, a.m, a.order);
     return a.src + bi * a.src_bstride + (y << Q) * E;
   };
-  tile_load<E, Q, true, NT>(r, src_tile(t), row_stride);
+  tile_load<E, Q, true, NT, CS && BITREV_LD_CS>(r, src_tile(t), row_stride);
   for (;;) {
     const uint64_t bi = t >> a.m, y = work_to_y(t & mmask, a.m, a.order);
     tile_stage<E, Q, NT>(r, smem);
     __syncthreads();
     const uint64_t tn = t + gridDim.x;
-    if (tn < a.ntiles) tile_load<E, Q, true, NT>(r, src_tile(tn), row_stride);
+    if (tn < a.ntiles) tile_load<E, Q, true, NT, CS && BITREV_LD_CS>(r, src_tile(tn), row_stride);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << Q) * E;
     tile_drain<E, Q, NT, CS>(smem, dbase, row_stride);
     if (tn >= a.ntiles) break;
@@ -436,7 +447,8 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
       const int c = id % T::CZ, g = id / T::CZ;
 #pragma unroll
       for (int k = 0; k < T::V; ++k)
-        r[it][k] = ld_stream(base + (uint64_t)(g + k * T::GX) * src_row + (uint64_t)c * 16);
+        r[it][k] = (CS && BITREV_LD_CS) ? ld_cs(base + (uint64_t)(g + k * T::GX) * src_row + (uint64_t)c * 16)
+                                        : ld_stream(base + (uint64_t)(g + k * T::GX) * src_row + (uint64_t)c * 16);
     }
   };
   // U[z][col]: ZS rows of GX chunks, chunk' = chunk ^ ((z >> LV) & 7)
@@ -591,8 +603,11 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
     cur_item(bi, y);
     const uint64_t ry = partner(y);
     const char* base = a.src + bi * a.src_bstride;
-    tile_load<E, Q, BITREV_IP_NC>(r0, base + (y << Q) * E, row_stride);
-    if (ry != y) tile_load<E, Q, BITREV_IP_NC>(r1, base + (ry << Q) * E, row_stride);
+    tile_load<E, Q, BITREV_IP_NC, BITREV_TILE_THREADS, CS && BITREV_LD_CS>(
+        r0, base + (y << Q) * E, row_stride);
+    if (ry != y)
+      tile_load<E, Q, BITREV_IP_NC, BITREV_TILE_THREADS, CS && BITREV_LD_CS>(
+          r1, base + (ry << Q) * E, row_stride);
   };
 
   if constexpr (COMPACT) pc.start(a); else skip_fwd();
@@ -664,8 +679,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, MINB)
   auto issue = [&]() {
     const uint64_t y = pair_from_index(pc.w, a.m), ry = dev_rev(y, a.m);
     if (rank && ry == y) return;  // palindrome: rank 0 alone
-    tile_load<E, Q, BITREV_IP_NC, NT>(r, a.src + pc.bi * a.src_bstride + ((rank ? ry : y) << Q) * E,
-                                      row_stride);
+    tile_load<E, Q, BITREV_IP_NC, NT, CS && BITREV_LD_CS>(
+        r, a.src + pc.bi * a.src_bstride + ((rank ? ry : y) << Q) * E, row_stride);
   };
   issue();
   for (;;) {
