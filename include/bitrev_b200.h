@@ -204,9 +204,11 @@ int bitrev_set_tile_path(int elem_bytes, int inplace, int path);
 /*
  * The (tile bits, staging path) of the calling thread's most recent
  * successful bitrev_oop / bitrev_inplace launch -- the choice tune_cobra's
- * report names for the reference (src/bench.py:380-433).  path -1 = whole-row
- * kernel (n*E <= 32 KB), -2 = element-wise kernel (unaligned views, 1/2-byte
- * elements); q is 0 for both.  With the knobs at their default values,
+ * report names for the reference (src/bench.py:380-433).  path -3 = short-row
+ * kernel (16-byte aligned rows of 4/8/16-byte elements, n*E <= 32 KB, many
+ * rows per CTA), -1 = whole-row kernel (other rows of n*E <= 32 KB), -2 =
+ * element-wise kernel (unaligned views, 1/2-byte elements); q is 0 for all
+ * three.  With the knobs at their default values,
  * launches below per-family byte budgets (8-64 MiB per side) use smaller
  * mid-size tiles: one large tile per SM leaves too few tiles to balance a
  * persistent grid there (tools/mid_sizes.py, mid_tier in bitrev_capi.cu).

@@ -110,7 +110,8 @@ def set_tile_path(elem_bytes: int, inplace: bool, path: int) -> None:
 
 def last_tile() -> tuple[int, int]:
     """(tile bits, staging path) of this thread's most recent bitrev_oop /
-    bitrev_inplace launch; path -1 = whole-row kernel, -2 = element-wise."""
+    bitrev_inplace launch; path -3 = short-row kernel, -1 = whole-row kernel,
+    -2 = element-wise."""
     q, path = ctypes.c_int(0), ctypes.c_int(0)
     call("bitrev_last_tile", ctypes.addressof(q), ctypes.addressof(path))
     return q.value, path.value

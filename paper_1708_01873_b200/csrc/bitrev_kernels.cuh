@@ -1590,6 +1590,88 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// short rows (n*E <= 32 KB, too short for a V x V tile): many rows per CTA
+//
+// One CTA iteration moves a 32 KB block of R = 32 KB / (n*E) consecutive
+// rows: 16-byte vector loads into registers (coalesced along each row), an
+// element scatter into shared memory at the bit-reversed position, a barrier,
+// then LDS.128 -> STG.128 of whole 16-byte output chunks.  The next block's
+// loads are issued before the drain.  A block's rows belong to this CTA alone,
+// so src == dst (in place) is safe.  Shared memory is swizzled per 16-byte
+// chunk: phys = c ^ ((c >> s) & 7), with s chosen so that the chunk bits that
+// vary across a warp's scatter (the top bits of rev(pos)) select different
+// bank groups; the linear drain stays conflict-free because the XOR term is
+// constant over every aligned group of 8 chunks (s >= 3).
+template <int E>
+struct Rows {
+  static constexpr int V = 16 / E;
+  static constexpr int LV = const_log2(V);
+  static constexpr int THREADS = 256;
+  static constexpr int BYTES = 32 * 1024;
+  static constexpr int NV = BYTES / 16 / THREADS;  // 16-byte vectors per thread per block
+};
+
+template <int E, bool INPLACE>
+__global__ void __launch_bounds__(Rows<E>::THREADS)
+    bitrev_rows_kernel(const char* src, char* dst, int b, int64_t batch, int64_t sbs,
+                       int64_t dbs, int s) {
+  using R = Rows<E>;
+  using W = typename Word<E>::T;
+  extern __shared__ __align__(16) uint4 smem[];
+  const int vb = b - R::LV;                        // vector-index bits per row
+  const int rb = const_log2(R::BYTES / 16) - vb;   // log2(rows per block)
+  const int64_t nblocks = (batch + (1ll << rb) - 1) >> rb;
+  auto phys = [&](int c) { return c ^ ((c >> s) & 7); };
+  uint4 r[R::NV];
+  auto load = [&](int64_t blk) {
+#pragma unroll
+    for (int j = 0; j < R::NV; ++j) {
+      const int v = j * R::THREADS + threadIdx.x;
+      const int64_t row = (blk << rb) + (v >> vb);
+      if (row < batch) {
+        const char* p = src + row * sbs + (int64_t)(v & ((1 << vb) - 1)) * 16;
+        r[j] = INPLACE ? ld_plain(p) : ld_stream(p);
+      }
+    }
+  };
+  int64_t blk = blockIdx.x;
+  if (blk >= nblocks) return;
+  load(blk);
+  for (;;) {
+    W* sw = reinterpret_cast<W*>(smem);
+#pragma unroll
+    for (int j = 0; j < R::NV; ++j) {
+      const int v = j * R::THREADS + threadIdx.x;
+      const int rl = v >> vb, pos = v & ((1 << vb) - 1);
+      const W* e = reinterpret_cast<const W*>(&r[j]);
+      const int rp = vb ? (int)(__brev((unsigned)pos) >> (32 - vb)) : 0;  // rev_{b-LV}(pos)
+#pragma unroll
+      for (int t = 0; t < R::V; ++t) {
+        // element pos*V + t lands at rev_b = rev_LV(t) * 2^(b-LV) + rev(pos)
+        const int rt = R::LV ? (int)(__brev((unsigned)t) >> (32 - R::LV)) : 0;
+        const int d = (rt << vb) + rp;                       // destination element in the row
+        const int c = (rl << vb) + (d >> R::LV);             // its 16-byte chunk in the block
+        sw[phys(c) * R::V + (d & (R::V - 1))] = e[t];
+      }
+    }
+    __syncthreads();
+    const int64_t nxt = blk + gridDim.x;
+    const int64_t base_row = blk << rb;
+    if (nxt < nblocks) load(nxt);
+#pragma unroll
+    for (int j = 0; j < R::NV; ++j) {
+      const int c = j * R::THREADS + threadIdx.x;
+      const int64_t row = base_row + (c >> vb);
+      if (row < batch)
+        st_vec(dst + row * dbs + (int64_t)(c & ((1 << vb) - 1)) * 16, smem[phys(c)]);
+    }
+    if (nxt >= nblocks) break;
+    __syncthreads();
+    blk = nxt;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // element-wise fallbacks (unaligned pointers, 1/2-byte elements): correct for
 // every width, not bandwidth-optimal.
 

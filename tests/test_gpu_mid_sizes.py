@@ -80,7 +80,10 @@ def test_pinned_tile_bits_disable_the_tiers(cuda, E, inplace):
 
 def test_last_tile_reports_row_and_elementwise_kernels(cuda):
     x = torch.arange(1 << 10, dtype=torch.int64, device=cuda)
-    br.cobra_in_place(x, br.CobraConfig(0), 10)  # 8 KB: whole-row kernel
+    br.cobra_in_place(x, br.CobraConfig(0), 10)  # 8 KB aligned rows: short-row kernel
+    assert br.last_tile() == (0, -3)
+    h = torch.arange(1 << 10, dtype=torch.int16, device=cuda)
+    br.cobra_in_place(h, br.CobraConfig(0), 10)  # 2-byte elements, 2 KB: whole-row kernel
     assert br.last_tile() == (0, -1)
     y = torch.arange(1 << 16, dtype=torch.int16, device=cuda)
     br.cobra_in_place(y, br.CobraConfig(0), 16)  # 2-byte elements: element-wise kernel

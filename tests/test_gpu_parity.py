@@ -116,6 +116,32 @@ def test_rect_out_of_place_tiles(cuda, E, q, b, batch):
         br.set_tile_path(E, False, old[1])
 
 
+@pytest.mark.parametrize("E", [4, 8, 16])
+@pytest.mark.parametrize("b,batch", [(2, 4097), (3, 1000), (5, 3), (7, 2049), (9, 130),
+                                     (11, 17), (12, 5), (13, 3)])
+@pytest.mark.parametrize("pad", [0, 16])
+def test_short_rows_kernel(cuda, E, b, batch, pad):
+    """Short rows (n*E <= 32 KB): many rows per CTA, partial last blocks,
+    padded row strides, in and out of place."""
+    if (E << b) > 32 * 1024 or (E << b) < 16:
+        pytest.skip("not a short-row case")
+    n = 1 << b
+    host = rand_bits((n + pad) * batch, E, seed=9000 + 100 * E + b).reshape(batch, n + pad)
+    expected = orc.oracle_permute(np.ascontiguousarray(host[:, :n]), b)
+    buf = torch.from_numpy(host.copy()).to(cuda)
+    rows = buf[:, :n]
+    out = torch.zeros(batch, n, dtype=buf.dtype, device=cuda)
+    br.bitrev_batched(rows, b, out)
+    assert br.last_tile() == (0, -3)
+    br.bitrev_batched_inplace(rows, b)
+    assert br.last_tile() == (0, -3)
+    torch.cuda.synchronize()
+    assert_same(out, expected)
+    assert_same(rows.contiguous(), expected)
+    if pad:  # padding between rows untouched
+        assert_same(buf[:, n:].contiguous(), np.ascontiguousarray(host[:, n:]))
+
+
 @pytest.mark.parametrize("E,q", [(4, 7), (8, 6), (8, 7), (16, 5), (16, 6)])
 @pytest.mark.parametrize("b,batch", [(14, 3), (15, 2), (17, 1), (20, 2), (23, 1)])
 def test_cluster_pair_tiles(cuda, E, q, b, batch):
