@@ -622,18 +622,18 @@ int launch_small(const void* src, void* dst, int b, int64_t batch, int64_t sbs, 
 
 // Short rows (n*E <= 32 KB) of 4/8/16-byte elements on 16-byte aligned rows:
 // many rows per CTA (bitrev_rows_kernel).  sbs/dbs in elements.
-template <int E>
+template <int E, int KB>
 int launch_rows(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
                 cudaStream_t st) {
-  using R = Rows<E>;
+  using R = Rows<E, KB>;
   const int vb = b - R::LV;
   if (vb < 0) return BITREV_ETILE;
-  const int rb = 11 - vb;  // log2(32 KB / 16 B) = 11
+  const int rb = const_log2(R::BYTES / 16) - vb;
   if (rb < 0) return BITREV_ETILE;
   const int64_t nblocks = (batch + (int64_t(1) << rb) - 1) >> rb;
   const int sh = vb - R::LV - 3 > 3 ? vb - R::LV - 3 : 3;
   const bool ip = src == dst;
-  auto kern = ip ? bitrev_rows_kernel<E, true> : bitrev_rows_kernel<E, false>;
+  auto kern = ip ? bitrev_rows_kernel<E, true, KB> : bitrev_rows_kernel<E, false, KB>;
   const int per_sm = prepare_kernel(kern, R::THREADS, R::BYTES);
   const int grid = grid_for((uint64_t)nblocks, per_sm);
   kern<<<grid, R::THREADS, R::BYTES, st>>>(static_cast<const char*>(src), static_cast<char*>(dst),
@@ -643,13 +643,20 @@ int launch_rows(const void* src, void* dst, int b, int64_t batch, int64_t sbs, i
 
 int dispatch_rows(int E, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
                   int64_t dbs, cudaStream_t st) {
-  switch (E) {
-    case 4: return launch_rows<4>(src, dst, b, batch, sbs, dbs, st);
-    case 8: return launch_rows<8>(src, dst, b, batch, sbs, dbs, st);
-    case 16: return launch_rows<16>(src, dst, b, batch, sbs, dbs, st);
+  const int64_t row = (int64_t)E << b;
+  // block = max(32 KB, one row); float32 rows of 128 KB would spill (not used)
+#define ROWS_E(EE, MAXKB)                                                                 \
+  if (E == EE) {                                                                          \
+    if (row <= 32 * 1024) return launch_rows<EE, 32>(src, dst, b, batch, sbs, dbs, st);   \
+    if (row <= 64 * 1024) return launch_rows<EE, 64>(src, dst, b, batch, sbs, dbs, st);   \
+    if constexpr (MAXKB >= 128)                                                           \
+      if (row <= 128 * 1024) return launch_rows<EE, 128>(src, dst, b, batch, sbs, dbs, st); \
   }
+  ROWS_E(4, 64) ROWS_E(8, 128) ROWS_E(16, 128)
+#undef ROWS_E
   return BITREV_ETILE;
 }
+
 
 int dispatch_small(int E, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
                    int64_t dbs, cudaStream_t st) {
@@ -755,6 +762,19 @@ Tier mid_tier(int E, bool inplace, uint64_t side_bytes) {
 }
 
 uint64_t side_bytes(int E, int b, int64_t batch) { return ((uint64_t)E << b) * (uint64_t)batch; }
+
+// In place, rows of 32-128 KB in large batches also take the short-row
+// kernel (a whole row staged in one CTA, 64/128 KB blocks): +6 % (float32,
+// 64 KB rows), +10-15 % (float64), +19-20 % (complex128) over tile pairs
+// (profiles/r01_short_rows.jsonl).  Out of place the tiles stay 2-6 % ahead,
+// float32 rows of 128 KB spill, and small batches would leave SMs idle (one
+// CTA per block), hence the limits.
+bool rows_inplace_ok(int E, int b, int64_t batch) {
+  if (E != 4 && E != 8 && E != 16) return false;
+  const int64_t row = (int64_t)E << b;
+  const int64_t cap = E == 4 ? 64 * 1024 : 128 * 1024;
+  return row > kSmallBytes && row <= cap && side_bytes(E, b, batch) >= (64ull << 20);
+}
 
 // Tile bits for the square kernels: the configured q, reduced so that
 // 2q <= b.  The dispatchers then walk further down to the largest
@@ -866,6 +886,10 @@ int bitrev_inplace(void* a, int b, int elem_bytes, int64_t batch, int64_t batch_
   if (batch == 1) batch_stride = n;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec_ok = aligned16(a) && ((batch_stride * E) % 16 == 0);
+  if (vec_ok && rows_inplace_ok(E, b, batch)) {
+    rc = dispatch_rows(E, a, a, b, batch, batch_stride, batch_stride, st);
+    if (rc != BITREV_ETILE) return note(rc, 0, -3);
+  }
   if (n * E <= kSmallBytes) {  // short rows: see bitrev_oop
     if (vec_ok && (E == 4 || E == 8 || E == 16)) {
       rc = dispatch_rows(E, a, a, b, batch, batch_stride, batch_stride, st);

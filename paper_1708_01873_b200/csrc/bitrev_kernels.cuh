@@ -1602,20 +1602,20 @@ __global__ void __launch_bounds__(256)
 // vary across a warp's scatter (the top bits of rev(pos)) select different
 // bank groups; the linear drain stays conflict-free because the XOR term is
 // constant over every aligned group of 8 chunks (s >= 3).
-template <int E>
+template <int E, int KB = 32>
 struct Rows {
   static constexpr int V = 16 / E;
   static constexpr int LV = const_log2(V);
   static constexpr int THREADS = 256;
-  static constexpr int BYTES = 32 * 1024;
+  static constexpr int BYTES = KB * 1024;
   static constexpr int NV = BYTES / 16 / THREADS;  // 16-byte vectors per thread per block
 };
 
-template <int E, bool INPLACE>
-__global__ void __launch_bounds__(Rows<E>::THREADS)
+template <int E, bool INPLACE, int KB = 32>
+__global__ void __launch_bounds__(Rows<E, KB>::THREADS)
     bitrev_rows_kernel(const char* src, char* dst, int b, int64_t batch, int64_t sbs,
                        int64_t dbs, int s) {
-  using R = Rows<E>;
+  using R = Rows<E, KB>;
   using W = typename Word<E>::T;
   extern __shared__ __align__(16) uint4 smem[];
   const int vb = b - R::LV;                        // vector-index bits per row

@@ -142,6 +142,24 @@ def test_short_rows_kernel(cuda, E, b, batch, pad):
         assert_same(buf[:, n:].contiguous(), np.ascontiguousarray(host[:, n:]))
 
 
+@pytest.mark.parametrize("E,b,batch", [(4, 14, 1024), (8, 13, 1024), (8, 14, 513),
+                                       (16, 12, 1025), (16, 13, 512)])
+def test_inplace_mid_rows_in_large_batches(cuda, E, b, batch):
+    """In place, rows of 64-128 KB in batches of >= 64 MiB take the short-row
+    kernel with one row per block (a whole row staged in one CTA)."""
+    n = 1 << b
+    pad = 16
+    host = rand_bits((n + pad) * batch, E, seed=9500 + 10 * E + b).reshape(batch, n + pad)
+    expected = orc.oracle_permute(np.ascontiguousarray(host[:, :n]), b)
+    buf = torch.from_numpy(host).to(cuda)
+    rows = buf[:, :n]
+    br.bitrev_batched_inplace(rows, b)
+    torch.cuda.synchronize()
+    assert br.last_tile() == (0, -3)
+    assert_same(rows.contiguous(), expected)
+    assert_same(buf[:, n:].contiguous(), np.ascontiguousarray(host[:, n:]))
+
+
 @pytest.mark.parametrize("E,q", [(4, 7), (8, 6), (8, 7), (16, 5), (16, 6)])
 @pytest.mark.parametrize("b,batch", [(14, 3), (15, 2), (17, 1), (20, 2), (23, 1)])
 def test_cluster_pair_tiles(cuda, E, q, b, batch):

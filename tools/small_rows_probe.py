@@ -12,7 +12,8 @@ import paper_1708_01873_b200 as br  # noqa: E402
 
 dev = torch.device("cuda", 0)
 for dt, E in ((torch.float32, 4), (torch.float64, 8), (torch.complex128, 16)):
-    for b in range(4, 15):
+    bits = [int(x) for x in sys.argv[1:]] or list(range(4, 15))
+    for b in bits:
         rows = 1 << (26 - b)
         x = torch.empty(rows, 1 << b, dtype=dt, device=dev)
         x.view(torch.uint8).random_()
