@@ -1180,6 +1180,25 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   a.batch = batch;
   a.src_bstride = src_batch_stride * E;
   a.dst_bstride = dst_batch_stride * E;
+  const bool rows_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
+                       ((dst_batch_stride * E) % 16 == 0) && b >= (E == 8 ? 1 : 0);
+  if (n * E <= kSmallBytes && rows_ok) {
+    // many short rows per CTA; the stages run on the staged block in shared
+    // memory (fft_rows_kernel)
+    const int lv = E == 8 ? 1 : 0;
+    const int vb = b - lv;
+    const int sh = vb - lv - 3 > 3 ? vb - lv - 3 : 3;
+    const int64_t nblocks = (batch + (int64_t(1) << (11 - vb)) - 1) >> (11 - vb);
+    const int smem = 32 * 1024 + (int)((n / 2) * E);
+    if (E == 8) {
+      const int per_sm = prepare_kernel(fft_rows_kernel<8>, 256, 48 * 1024);
+      fft_rows_kernel<8><<<grid_for((uint64_t)nblocks, per_sm), 256, smem, st>>>(fa, sh);
+    } else {
+      const int per_sm = prepare_kernel(fft_rows_kernel<16>, 256, 48 * 1024);
+      fft_rows_kernel<16><<<grid_for((uint64_t)nblocks, per_sm), 256, smem, st>>>(fa, sh);
+    }
+    return finish_launch();
+  }
   if (n * E <= kSmallBytes) {
     const int bytes = (int)(n * E);
     const int grid = grid_for((uint64_t)batch, 8);

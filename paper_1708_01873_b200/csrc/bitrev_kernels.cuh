@@ -1564,6 +1564,115 @@ __global__ void __launch_bounds__(256) fft_prepass_small_kernel(FftArgs fa) {
   }
 }
 
+// Geometry of the short-row kernels (bitrev_rows_kernel, fft_rows_kernel):
+// KB-kilobyte blocks of consecutive rows, 256 threads, NV 16-byte vectors per
+// thread.
+template <int E, int KB = 32>
+struct Rows {
+  static constexpr int V = 16 / E;
+  static constexpr int LV = const_log2(V);
+  static constexpr int THREADS = 256;
+  static constexpr int BYTES = KB * 1024;
+  static constexpr int NV = BYTES / 16 / THREADS;  // 16-byte vectors per thread per block
+};
+
+// ---------------------------------------------------------------------------
+// FFT pre-pass on short rows (n*E <= 32 KB, 16-byte aligned): many rows per
+// CTA, as bitrev_rows_kernel -- a 32 KB block of rows is loaded with 16-byte
+// vectors and scattered bit-reversed into shared memory; then the requested
+// radix-2 DIT stages run on the block in shared memory (one barrier per stage
+// for the whole block, not per row); then LDS.128 -> STG.128.  Twiddles
+// W_n^j (j < n/2) are computed once per CTA in double precision into a shared
+// table; stage s uses W_{2^s}^k = W_n^(k * 2^(b-s)).
+
+#ifndef BITREV_FFT_ROWS_MINB16
+#define BITREV_FFT_ROWS_MINB16 3
+#endif
+#ifndef BITREV_FFT_ROWS_MINB8
+#define BITREV_FFT_ROWS_MINB8 1
+#endif
+template <int E>
+__global__ void __launch_bounds__(256, E == 16 ? BITREV_FFT_ROWS_MINB16 : BITREV_FFT_ROWS_MINB8)
+    fft_rows_kernel(FftArgs fa, int swz) {
+  using C = typename Cplx<E>::T;
+  using Rl = typename Cplx<E>::R;
+  using R = Rows<E, 32>;
+  extern __shared__ __align__(16) uint4 smem[];
+  C* tw = reinterpret_cast<C*>(reinterpret_cast<char*>(smem) + R::BYTES);
+  const TileArgs& a = fa.t;
+  const int b = a.b, half_n = 1 << (b - 1);
+  const int vb = b - R::LV;
+  const int rb = const_log2(R::BYTES / 16) - vb;
+  const int64_t nblocks = (a.batch + (1ll << rb) - 1) >> rb;
+  auto phys = [&](int c) { return c ^ ((c >> swz) & 7); };
+  C* sc = reinterpret_cast<C*>(smem);
+  // element d of block row rl, through the 16-byte chunk swizzle
+  auto at = [&](int rl, int d) -> C& {
+    return sc[phys((rl << vb) + (d >> R::LV)) * R::V + (d & (R::V - 1))];
+  };
+  int64_t blk = blockIdx.x;
+  if (blk >= nblocks) return;
+  for (int j = threadIdx.x; j < half_n; j += R::THREADS) {
+    double sn, cs;
+    sincospi((fa.inverse ? 2.0 : -2.0) * j / (2 * half_n), &sn, &cs);
+    tw[j] = C{(Rl)cs, (Rl)sn};
+  }
+  uint4 r[R::NV];
+  auto load = [&](int64_t k) {
+#pragma unroll
+    for (int j = 0; j < R::NV; ++j) {
+      const int v = j * R::THREADS + threadIdx.x;
+      const int64_t row = (k << rb) + (v >> vb);
+      if (row < a.batch)
+        r[j] = ld_stream(a.src + row * a.src_bstride + (int64_t)(v & ((1 << vb) - 1)) * 16);
+    }
+  };
+  load(blk);
+  for (;;) {
+#pragma unroll
+    for (int j = 0; j < R::NV; ++j) {
+      const int v = j * R::THREADS + threadIdx.x;
+      const int rl = v >> vb, pos = v & ((1 << vb) - 1);
+      const C* e = reinterpret_cast<const C*>(&r[j]);
+      const int rp = vb ? (int)(__brev((unsigned)pos) >> (32 - vb)) : 0;
+#pragma unroll
+      for (int t = 0; t < R::V; ++t) {
+        const int rt = R::LV ? (int)(__brev((unsigned)t) >> (32 - R::LV)) : 0;
+        at(rl, (rt << vb) + rp) = e[t];
+      }
+    }
+    __syncthreads();
+    const int64_t nxt = blk + gridDim.x;
+    const int64_t base_row = blk << rb;
+    if (nxt < nblocks) load(nxt);
+    const int nbf = 1 << (rb + b - 1);  // butterflies per stage in the block
+    for (int st = 1; st <= fa.stages; ++st) {
+      const int half = 1 << (st - 1);
+      for (int k = threadIdx.x; k < nbf; k += R::THREADS) {
+        const int rl = k >> (b - 1), t = k & (half_n - 1);
+        const int kk = t & (half - 1);
+        const int i0 = ((t >> (st - 1)) << st) + kk;
+        C& p0 = at(rl, i0);
+        C& p1 = at(rl, i0 + half);
+        const C u = p0, v = cmul(p1, tw[kk << (b - st)]);
+        p0 = cadd(u, v);
+        p1 = csub(u, v);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < R::NV; ++j) {
+      const int c = j * R::THREADS + threadIdx.x;
+      const int64_t row = base_row + (c >> vb);
+      if (row < a.batch)
+        st_vec(a.dst + row * a.dst_bstride + (int64_t)(c & ((1 << vb) - 1)) * 16, smem[phys(c)]);
+    }
+    if (nxt >= nblocks) break;
+    __syncthreads();
+    blk = nxt;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // whole-row-in-shared-memory kernel for small n (n*E <= kSmallBytes); one CTA
 // per batch row, grid-stride over rows.  Works in place (src == dst) because
@@ -1602,15 +1711,6 @@ __global__ void __launch_bounds__(256)
 // vary across a warp's scatter (the top bits of rev(pos)) select different
 // bank groups; the linear drain stays conflict-free because the XOR term is
 // constant over every aligned group of 8 chunks (s >= 3).
-template <int E, int KB = 32>
-struct Rows {
-  static constexpr int V = 16 / E;
-  static constexpr int LV = const_log2(V);
-  static constexpr int THREADS = 256;
-  static constexpr int BYTES = KB * 1024;
-  static constexpr int NV = BYTES / 16 / THREADS;  // 16-byte vectors per thread per block
-};
-
 template <int E, bool INPLACE, int KB = 32>
 __global__ void __launch_bounds__(Rows<E, KB>::THREADS)
     bitrev_rows_kernel(const char* src, char* dst, int b, int64_t batch, int64_t sbs,
