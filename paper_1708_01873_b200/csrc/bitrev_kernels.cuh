@@ -1580,8 +1580,9 @@ struct Rows {
 // FFT pre-pass on short rows (n*E <= 32 KB, 16-byte aligned): many rows per
 // CTA, as bitrev_rows_kernel -- a 32 KB block of rows is loaded with 16-byte
 // vectors and scattered bit-reversed into shared memory; then the requested
-// radix-2 DIT stages run on the block in shared memory (one barrier per stage
-// for the whole block, not per row); then LDS.128 -> STG.128.  Twiddles
+// radix-2 DIT stages run on the block in shared memory, paired into radix-4
+// passes (one barrier per pass for the whole block, not per row); then
+// LDS.128 -> STG.128.  Twiddles
 // W_n^j (j < n/2) are computed once per CTA in double precision into a shared
 // table; stage s uses W_{2^s}^k = W_n^(k * 2^(b-s)).
 
@@ -1646,7 +1647,45 @@ __global__ void __launch_bounds__(256, E == 16 ? BITREV_FFT_ROWS_MINB16 : BITREV
     const int64_t base_row = blk << rb;
     if (nxt < nblocks) load(nxt);
     const int nbf = 1 << (rb + b - 1);  // butterflies per stage in the block
-    for (int st = 1; st <= fa.stages; ++st) {
+    int st0 = 1;
+    // stage pairs (s, s+1) as radix-4 passes: a thread owns the quad
+    // (k, k+h, k+2h, k+3h) of an aligned 4h block, h = 2^(s-1); stage s pairs
+    // (k, k+h) and (k+2h, k+3h) with W_{2h}^kk, stage s+1 pairs (k, k+2h) with
+    // W_{4h}^kk and (k+h, k+3h) with W_{4h}^(kk+h): half the shared-memory
+    // passes and barriers of radix-2
+    for (; st0 + 1 <= fa.stages; st0 += 2) {
+      const int h = 1 << (st0 - 1);
+      const int nq = nbf >> 1;
+      for (int q = threadIdx.x; q < nq; q += R::THREADS) {
+        const int rl = q >> (b - 2), t = q & ((half_n >> 1) - 1);
+        const int kk = t & (h - 1);
+        const int i0 = ((t >> (st0 - 1)) << (st0 + 1)) + kk;
+        C& p0 = at(rl, i0);
+        C& p1 = at(rl, i0 + h);
+        C& p2 = at(rl, i0 + 2 * h);
+        C& p3 = at(rl, i0 + 3 * h);
+        C x0 = p0, x1 = p1, x2 = p2, x3 = p3;
+        const C w1 = tw[kk << (b - st0)];
+        C v = cmul(x1, w1);
+        x1 = csub(x0, v);
+        x0 = cadd(x0, v);
+        v = cmul(x3, w1);
+        x3 = csub(x2, v);
+        x2 = cadd(x2, v);
+        v = cmul(x2, tw[kk << (b - st0 - 1)]);
+        x2 = csub(x0, v);
+        x0 = cadd(x0, v);
+        v = cmul(x3, tw[(kk + h) << (b - st0 - 1)]);
+        x3 = csub(x1, v);
+        x1 = cadd(x1, v);
+        p0 = x0;
+        p1 = x1;
+        p2 = x2;
+        p3 = x3;
+      }
+      __syncthreads();
+    }
+    for (int st = st0; st <= fa.stages; ++st) {  // an odd last stage: radix 2
       const int half = 1 << (st - 1);
       for (int k = threadIdx.x; k < nbf; k += R::THREADS) {
         const int rl = k >> (b - 1), t = k & (half_n - 1);
