@@ -1190,13 +1190,11 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     const int sh = vb - lv - 3 > 3 ? vb - lv - 3 : 3;
     const int64_t nblocks = (batch + (int64_t(1) << (11 - vb)) - 1) >> (11 - vb);
     const int smem = 32 * 1024 + (int)((n / 2) * E);
-    if (E == 8) {
-      const int per_sm = prepare_kernel(fft_rows_kernel<8>, 256, 48 * 1024);
-      fft_rows_kernel<8><<<grid_for((uint64_t)nblocks, per_sm), 256, smem, st>>>(fa, sh);
-    } else {
-      const int per_sm = prepare_kernel(fft_rows_kernel<16>, 256, 48 * 1024);
-      fft_rows_kernel<16><<<grid_for((uint64_t)nblocks, per_sm), 256, smem, st>>>(fa, sh);
-    }
+    // rotated quad order for longer rows (profiles/r01_short_row_fft.jsonl)
+    auto kern = E == 8 ? (b >= 10 ? fft_rows_kernel<8, true> : fft_rows_kernel<8, false>)
+                       : (b >= 8 ? fft_rows_kernel<16, true> : fft_rows_kernel<16, false>);
+    const int per_sm = prepare_kernel(kern, 256, 48 * 1024);
+    kern<<<grid_for((uint64_t)nblocks, per_sm), 256, smem, st>>>(fa, sh);
     return finish_launch();
   }
   if (n * E <= kSmallBytes) {

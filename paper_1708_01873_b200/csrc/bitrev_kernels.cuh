@@ -1590,9 +1590,29 @@ struct Rows {
 #define BITREV_FFT_ROWS_MINB16 3
 #endif
 #ifndef BITREV_FFT_ROWS_MINB8
-#define BITREV_FFT_ROWS_MINB8 1
+#define BITREV_FFT_ROWS_MINB8 2
 #endif
-template <int E>
+// Rotate a 4-array right by r (runtime): a[m] <- a[(m - r) & 3], as selects.
+template <typename C>
+__device__ __forceinline__ void rot4(C (&a)[4], int r) {
+  if (r & 1) {
+    const C t = a[3];
+    a[3] = a[2];
+    a[2] = a[1];
+    a[1] = a[0];
+    a[0] = t;
+  }
+  if (r & 2) {
+    C t = a[0];
+    a[0] = a[2];
+    a[2] = t;
+    t = a[1];
+    a[1] = a[3];
+    a[3] = t;
+  }
+}
+
+template <int E, bool ROT>
 __global__ void __launch_bounds__(256, E == 16 ? BITREV_FFT_ROWS_MINB16 : BITREV_FFT_ROWS_MINB8)
     fft_rows_kernel(FftArgs fa, int swz) {
   using C = typename Cplx<E>::T;
@@ -1660,11 +1680,16 @@ __global__ void __launch_bounds__(256, E == 16 ? BITREV_FFT_ROWS_MINB16 : BITREV
         const int rl = q >> (b - 2), t = q & ((half_n >> 1) - 1);
         const int kk = t & (h - 1);
         const int i0 = ((t >> (st0 - 1)) << (st0 + 1)) + kk;
-        C& p0 = at(rl, i0);
-        C& p1 = at(rl, i0 + h);
-        C& p2 = at(rl, i0 + 2 * h);
-        C& p3 = at(rl, i0 + 3 * h);
-        C x0 = p0, x1 = p1, x2 = p2, x3 = p3;
+        // ROT (longer rows): access the quad in an order rotated by rot -- with
+        // small h the lanes of one wavefront (16 for 8-byte, 8 for 16-byte
+        // elements) would hit only 4 (resp. 2) of the bank slots.  Shorter
+        // rows are already spread by the chunk swizzle and skip the selects.
+        const int rot = ROT ? ((E == 8 ? (q >> 2) : (q >> 1)) & 3) : 0;
+        C x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = at(rl, i0 + ((j + rot) & 3) * h);
+        if constexpr (ROT) rot4(x, rot);  // x[m] = element i0 + m*h
+        C x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
         const C w1 = tw[kk << (b - st0)];
         C v = cmul(x1, w1);
         x1 = csub(x0, v);
@@ -1678,10 +1703,13 @@ __global__ void __launch_bounds__(256, E == 16 ? BITREV_FFT_ROWS_MINB16 : BITREV
         v = cmul(x3, tw[(kk + h) << (b - st0 - 1)]);
         x3 = csub(x1, v);
         x1 = cadd(x1, v);
-        p0 = x0;
-        p1 = x1;
-        p2 = x2;
-        p3 = x3;
+        x[0] = x0;
+        x[1] = x1;
+        x[2] = x2;
+        x[3] = x3;
+        if constexpr (ROT) rot4(x, (4 - rot) & 3);  // x[j] = element i0 + ((j + rot) & 3)*h
+#pragma unroll
+        for (int j = 0; j < 4; ++j) at(rl, i0 + ((j + rot) & 3) * h) = x[j];
       }
       __syncthreads();
     }
