@@ -64,7 +64,10 @@
 #define BITREV_CPA_STAGES 3  // pair stages of the cp.async in-place kernel
 #endif
 #ifndef BITREV_FFT_MINB
-#define BITREV_FFT_MINB 1  // min CTAs/SM for the 5..7-stage FFT kernels (register cap)
+#define BITREV_FFT_MINB 3  // min CTAs/SM for the many-stage FFT kernels (register cap)
+#endif
+#ifndef BITREV_FFT_MINB_FROM
+#define BITREV_FFT_MINB_FROM 3  // ... from this many fused stages on
 #endif
 #ifndef BITREV_RING_BUDGET_KB
 #define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
@@ -1462,14 +1465,20 @@ __device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_
       }
     }
   };
-  constexpr int LF = stages <= 2 ? 0 : stages <= 4 ? 1 : stages <= 6 ? 2 : 3;  // final layout
+  // final layout.  complex64 after 3-4 stages: layout B stores 32-byte runs
+  // per group of 4 lanes; one more exchange into layout C gives 128-byte runs
+  // (+11 % at 4 stages).  complex128's layout-B runs are already 64 bytes and
+  // the exchange costs more than it saves (-2.6 %).
+  constexpr bool kBtoC = E == 8 && stages >= 3 && stages <= 4;
+  if constexpr (kBtoC) to_layout(2);
+  constexpr int LF = stages <= 2 ? 0 : stages <= 4 ? (kBtoC ? 2 : 1) : stages <= 6 ? 2 : 3;
   store(std::integral_constant<int, LF>{});
   (void)L;
 }
 
 // Rectangular-tile FFT pre-pass (bitrev_oop_rect_kernel's load/stage path).
 template <int E, int QX, int QZ, int STAGES>
-__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS, STAGES >= 5 ? BITREV_FFT_MINB : 1)
+__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS, STAGES >= BITREV_FFT_MINB_FROM ? BITREV_FFT_MINB : 1)
     bitrev_fft_rect_kernel(FftArgs fa) {
   using T = Rect<E, QX, QZ>;
   using C = typename Cplx<E>::T;
