@@ -28,14 +28,15 @@ std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_q_oop[17];
 std::atomic<int> g_q_ip[17];
 
-// Defaults from tools/tune_all.py / tools/oop_sizes.py on B200 (interleaved
-// rounds; profiles/tune_r01*.jsonl): tile bits Q and staging path per
-// (E, family).
+// Large-size defaults, measured on B200 with interleaved rounds (tools/
+// tune_all.py, rect_qz.py, sweep.py; profiles/tune_r01*, r01_rect_qz*,
+// r01_inplace_cluster_ab): tile bits Q and staging path per (E, family).
+// Smaller launches are re-routed by mid_tier and by the short-row kernels.
 int default_q(int E, bool inplace) {
   switch (E) {
     case 4: return inplace ? 6 : 8;   // out of place: rectangular QX = 8 (path 3)
     case 8: return inplace ? 6 : 7;   // out of place: rectangular QX = 7 (path 3)
-    case 16: return 6;                // in place: 2-CTA cluster pairs (path 6)
+    case 16: return 6;                // 1 KB rows: square tiles / in place 2-CTA cluster pairs
     default: return 0;
   }
 }
@@ -64,9 +65,11 @@ int env_int(const char* name, int dflt) {
 
 std::atomic<int> g_order_oop{-1}, g_order_ip{-1};
 
-// Staging path per (element size, family): 0 = register (LDG/STS), 1 = TMA
-// bulk ring (cp.async.bulk + mbarrier).  -1 = not yet read from the
-// environment (BITREV_B200_PATH_OOP / BITREV_B200_PATH_IP), else default.
+// Staging path per (element size, family): 0 = register tiles (LDG/STS),
+// 1 = TMA bulk ring, 2 = TMA tensor ring, 3 = rectangular tiles (out of
+// place), 4 = cp.async pairs, 5 = TMA-store pairs, 6 = 2-CTA cluster pairs
+// (in place).  -1 = not yet read from the environment (BITREV_B200_PATH_OOP /
+// BITREV_B200_PATH_IP), else default.
 std::atomic<int> g_path_oop[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 std::atomic<int> g_path_ip[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 
