@@ -142,10 +142,11 @@ int bitrev_apply_pairs(void* a, const void* pairs, int64_t npairs, int elem_byte
  * stages applied to bit-reversed src, per row (complex64: elem_bytes 8,
  * complex128: 16; forward twiddles exp(-2 pi i k / 2^s), or conjugated when
  * inverse != 0, no normalisation).  stages = 0 is the plain permutation;
- * stages = b is a complete unnormalised radix-2 FFT.  Rows of n*E <= 32 KB
- * take any stages <= b; larger rows fuse up to 7 (complex64) or 6
- * (complex128) stages into the drain of rectangular tiles whose destination
- * rows are the FFT blocks, at the permutation's HBM traffic.
+ * stages = b is a complete unnormalised radix-2 FFT.  Rows of n*E <= 64 KB
+ * (16-byte aligned; 32 KB otherwise) take any stages <= b; larger rows fuse
+ * up to 7 (complex64) or 6 (complex128) stages into the drain of rectangular
+ * tiles whose destination rows are the FFT blocks, at the permutation's HBM
+ * traffic.
  * Serves the downstream step the reference's permutation exists for
  * (SURVEY.md 8(f) f2).  No reference counterpart.
  */

@@ -1185,18 +1185,27 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   a.dst_bstride = dst_batch_stride * E;
   const bool rows_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                        ((dst_batch_stride * E) % 16 == 0) && b >= (E == 8 ? 1 : 0);
-  if (n * E <= kSmallBytes && rows_ok) {
-    // many short rows per CTA; the stages run on the staged block in shared
-    // memory (fft_rows_kernel)
+  // rows of 64 KB take the staged-row kernel only for more stages than the
+  // tiles fuse (a complete FFT of the row): for <= 7 / 6 stages the tiles run
+  // 6.1-6.4 TB/s against 1.7-5.2 (tools/fft64_probe.py)
+  const int tile_stages = E == 8 ? 7 : 6;
+  if (rows_ok && (n * E <= kSmallBytes || (n * E <= 2 * kSmallBytes && stages > tile_stages))) {
+    // many short rows per CTA (one row per CTA for 64 KB rows); the stages run
+    // on the staged block in shared memory (fft_rows_kernel)
     const int lv = E == 8 ? 1 : 0;
     const int vb = b - lv;
     const int sh = vb - lv - 3 > 3 ? vb - lv - 3 : 3;
-    const int64_t nblocks = (batch + (int64_t(1) << (11 - vb)) - 1) >> (11 - vb);
-    const int smem = 32 * 1024 + (int)((n / 2) * E);
+    const bool big = n * E > kSmallBytes;
+    const int lblk = big ? 12 : 11;  // log2(block bytes / 16)
+    const int64_t nblocks = (batch + (int64_t(1) << (lblk - vb)) - 1) >> (lblk - vb);
+    const int blk_bytes = big ? 2 * kSmallBytes : kSmallBytes;
+    const int smem = blk_bytes + (int)((n / 2) * E);
     // rotated quad order for longer rows (profiles/r01_short_row_fft.jsonl)
-    auto kern = E == 8 ? (b >= 10 ? fft_rows_kernel<8, true> : fft_rows_kernel<8, false>)
-                       : (b >= 8 ? fft_rows_kernel<16, true> : fft_rows_kernel<16, false>);
-    const int per_sm = prepare_kernel(kern, 256, 48 * 1024);
+    const bool rot = E == 8 ? b >= 10 : b >= 8;
+    auto kern = big ? (E == 8 ? fft_rows_kernel<8, true, 64> : fft_rows_kernel<16, true, 64>)
+                    : (E == 8 ? (rot ? fft_rows_kernel<8, true> : fft_rows_kernel<8, false>)
+                              : (rot ? fft_rows_kernel<16, true> : fft_rows_kernel<16, false>));
+    const int per_sm = prepare_kernel(kern, 256, blk_bytes + blk_bytes / 2);
     kern<<<grid_for((uint64_t)nblocks, per_sm), 256, smem, st>>>(fa, sh);
     return finish_launch();
   }

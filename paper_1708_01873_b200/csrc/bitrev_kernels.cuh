@@ -1621,12 +1621,12 @@ __device__ __forceinline__ void rot4(C (&a)[4], int r) {
   }
 }
 
-template <int E, bool ROT>
-__global__ void __launch_bounds__(256, E == 16 ? BITREV_FFT_ROWS_MINB16 : BITREV_FFT_ROWS_MINB8)
+template <int E, bool ROT, int KB = 32>
+__global__ void __launch_bounds__(256, KB > 32 ? 2 : (E == 16 ? BITREV_FFT_ROWS_MINB16 : BITREV_FFT_ROWS_MINB8))
     fft_rows_kernel(FftArgs fa, int swz) {
   using C = typename Cplx<E>::T;
   using Rl = typename Cplx<E>::R;
-  using R = Rows<E, 32>;
+  using R = Rows<E, KB>;
   extern __shared__ __align__(16) uint4 smem[];
   C* tw = reinterpret_cast<C*>(reinterpret_cast<char*>(smem) + R::BYTES);
   const TileArgs& a = fa.t;

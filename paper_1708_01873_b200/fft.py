@@ -5,7 +5,7 @@ The permutation is the first step of an iterative decimation-in-time FFT
 outputs, which are exactly the destination rows of the tile kernels, so
 bitrev_dit_prepass runs them in the tile drain at the permutation's HBM
 traffic: up to 7 stages for complex64, 6 for complex128.
-Rows of at most 32 KB take any number of stages, so stages = b gives a
+Rows of at most 64 KB take any number of stages, so stages = b gives a
 complete (unnormalised) radix-2 FFT.
 """
 
@@ -60,7 +60,9 @@ def bitrev_dit_prepass(x, b: int, stages: int, inverse: bool = False, out=None) 
 
 
 def max_fused_stages(b: int, elem_bytes: int) -> int:
-    """Stages the fused path accepts for a row of 2^b elements."""
-    if (1 << b) * elem_bytes <= 32 * 1024:
+    """Stages the fused path accepts for a row of 2^b elements: all of them
+    (a complete FFT) for rows up to 64 KB, else 7 (complex64) / 6
+    (complex128)."""
+    if (1 << b) * elem_bytes <= 64 * 1024:
         return b
     return 7 if elem_bytes == 8 else 6

@@ -53,10 +53,11 @@ def test_fused_stages_match_reference(cuda, dtype, b, stages, inverse):
 
 
 @pytest.mark.parametrize("dtype", [torch.complex64, torch.complex128])
-@pytest.mark.parametrize("b", [1, 2, 5, 8, 11])
+@pytest.mark.parametrize("b", [1, 2, 5, 8, 11, 12, 13])
 def test_small_rows_full_fft(cuda, dtype, b):
-    if (1 << b) * (8 if dtype == torch.complex64 else 16) > 32768:
-        pytest.skip("row does not fit the small path")
+    """Rows up to 64 KB take any number of stages: a complete FFT."""
+    if (1 << b) * (8 if dtype == torch.complex64 else 16) > 65536:
+        pytest.skip("row too long for a complete fused FFT")
     x = rand_complex((3, 1 << b), dtype, b)
     got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, b)
     check(got, np.fft.fft(x.astype(np.complex128), axis=-1), dtype, b)
