@@ -647,9 +647,12 @@ int launch_rows(const void* src, void* dst, int b, int64_t batch, int64_t sbs, i
 int dispatch_rows(int E, const void* src, void* dst, int b, int64_t batch, int64_t sbs,
                   int64_t dbs, cudaStream_t st) {
   const int64_t row = (int64_t)E << b;
-  // block = max(32 KB, one row); float32 rows of 128 KB would spill (not used)
+  // block: 16 KB for 8/16-byte elements, 32 KB for 4-byte ones (measured,
+  // profiles/r01_short_rows_blocks.txt: +3-5 % and best respectively), or one
+  // whole row when it is longer; float32 rows of 128 KB would spill (unused)
 #define ROWS_E(EE, MAXKB)                                                                 \
   if (E == EE) {                                                                          \
+    if (EE != 4 && row <= 16 * 1024) return launch_rows<EE, 16>(src, dst, b, batch, sbs, dbs, st); \
     if (row <= 32 * 1024) return launch_rows<EE, 32>(src, dst, b, batch, sbs, dbs, st);   \
     if (row <= 64 * 1024) return launch_rows<EE, 64>(src, dst, b, batch, sbs, dbs, st);   \
     if constexpr (MAXKB >= 128)                                                           \
