@@ -1199,13 +1199,18 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     const int vb = b - lv;
     const int sh = vb - lv - 3 > 3 ? vb - lv - 3 : 3;
     const bool big = n * E > kSmallBytes;
-    const int lblk = big ? 12 : 11;  // log2(block bytes / 16)
+    // 16 KB blocks for rows up to 16 KB: +1-6 % over 32 KB blocks
+    // (profiles/r01_short_row_fft.jsonl history in DESIGN.md)
+    const bool small16 = n * E <= kSmallBytes / 2;
+    const int lblk = big ? 12 : (small16 ? 10 : 11);  // log2(block bytes / 16)
     const int64_t nblocks = (batch + (int64_t(1) << (lblk - vb)) - 1) >> (lblk - vb);
-    const int blk_bytes = big ? 2 * kSmallBytes : kSmallBytes;
+    const int blk_bytes = big ? 2 * kSmallBytes : (small16 ? kSmallBytes / 2 : kSmallBytes);
     const int smem = blk_bytes + (int)((n / 2) * E);
     // rotated quad order for longer rows (profiles/r01_short_row_fft.jsonl)
     const bool rot = E == 8 ? b >= 10 : b >= 8;
     auto kern = big ? (E == 8 ? fft_rows_kernel<8, true, 64> : fft_rows_kernel<16, true, 64>)
+              : small16 ? (E == 8 ? (rot ? fft_rows_kernel<8, true, 16> : fft_rows_kernel<8, false, 16>)
+                                  : (rot ? fft_rows_kernel<16, true, 16> : fft_rows_kernel<16, false, 16>))
                     : (E == 8 ? (rot ? fft_rows_kernel<8, true> : fft_rows_kernel<8, false>)
                               : (rot ? fft_rows_kernel<16, true> : fft_rows_kernel<16, false>));
     const int per_sm = prepare_kernel(kern, 256, blk_bytes + blk_bytes / 2);
