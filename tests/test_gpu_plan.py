@@ -39,14 +39,19 @@ def test_inplace_and_oop_plans(cuda, b, batch, dtype):
         assert torch.equal(x.view(torch.uint8), ref.view(torch.uint8))
 
 
-def test_fft_plan(cuda):
-    b = 14
-    x = torch.randn(4, 1 << b, dtype=torch.complex64, device=cuda)
+@pytest.mark.parametrize("b,batch,stages,dtype", [
+    (14, 4, 7, torch.complex64),      # fused tiles
+    (8, 32, 8, torch.complex64),      # short rows: complete FFT, many rows per CTA
+    (13, 3, 13, torch.complex64),     # 64 KB rows: complete FFT, one row per CTA
+    (10, 16, 10, torch.complex128),
+])
+def test_fft_plan(cuda, b, batch, stages, dtype):
+    x = torch.randn(batch, 1 << b, dtype=dtype, device=cuda)
     y = torch.empty_like(x)
-    plan = br.make_plan(x, b, y, stages=7)
+    plan = br.make_plan(x, b, y, stages=stages)
     plan.replay()
     torch.cuda.synchronize()
-    ref = br.bitrev_dit_prepass(x, b, 7)
+    ref = br.bitrev_dit_prepass(x, b, stages)
     assert torch.equal(y, ref)
 
 
