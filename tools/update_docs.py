@@ -76,17 +76,17 @@ def main():
     readme = (ROOT / "README.md").read_text()
     readme = replace_table(readme, "| in place 2^26 float64 (headline)", [
         f"| in place 2^26 float64 (headline) | {f('cfg2')['value']:.0f} | "
-        f"{f('cfg2')['roofline']['frac']:.2f} |",
+        f"{f('cfg2')['roofline']['frac']:.3f} |",
         "| out of place 2^30 float32 / float64 / complex128 | "
         + " / ".join(f"{f(w)['value']:.0f}" for w in ("cfg3-4", "cfg3-8", "cfg3-16")) + " | "
-        + " / ".join(f"{f(w)['roofline']['frac']:.2f}" for w in ("cfg3-4", "cfg3-8", "cfg3-16"))
+        + " / ".join(f"{f(w)['roofline']['frac']:.3f}" for w in ("cfg3-4", "cfg3-8", "cfg3-16"))
         + " |",
         f"| batched 4096 × 2^16 complex64 | {f('cfg4')['value']:.0f} | "
-        f"{f('cfg4')['roofline']['frac']:.2f} |",
+        f"{f('cfg4')['roofline']['frac']:.3f} |",
         f"| same + 7 fused FFT butterfly stages | {f('cfg4-fft7')['value']:.0f} | "
-        f"{f('cfg4-fft7')['roofline']['frac']:.2f} |",
+        f"{f('cfg4-fft7')['roofline']['frac']:.3f} |",
         f"| out of place 2^20 complex128 (33 MB, launch/latency bound) | "
-        f"{f('cfg1')['value']:.0f} | {f('cfg1')['roofline']['frac']:.2f} |",
+        f"{f('cfg1')['value']:.0f} | {f('cfg1')['roofline']['frac']:.3f} |",
     ])
     (ROOT / "README.md").write_text(readme)
 
