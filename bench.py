@@ -2,31 +2,43 @@
 """Benchmark: effective HBM GB/s (2*n*elem_bytes / time) of the bit-reversed
 permutation on B200, plus the reference's CPU path timed on the host cores.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload W]
                     [--impl ours|reference]
 
 A "step" is one permutation of one batch of synthetic input (BASELINE.json
-configs; default cfg2 = the in-place tile-pair swap of n=2^26 float64, the
-configuration the headline metric is quoted on).  Timing: W untimed warm-up
-steps, then EXACTLY K steps, each bracketed by CUDA events on the stream the
-kernel is launched on, with a barrier + device synchronise on both sides; the
-per-rank time is the sum of the K step durations and the job time is the max
-over ranks.  Workloads whose working set is below 4x the L2 get an L2 flush
-(a 512 MiB write) before every step, outside the step's events.
+configs).  BASELINE.json quotes its metric "vs log2 n" on no single config,
+so the N=1 line is the largest single-GPU config: cfg3-16 = n=2^30 complex128
+out of place (16 GiB per side); the same line carries cfg3-4 / cfg3-8 (the
+element-width sweep of config 3) under "width_sweep".  With N > 1 the default
+is cfg5, the one config that shards a single array: n=2^32 complex64 split by
+its top log2 N index bits, local reversal + NCCL all_to_all_single over
+NVLink + local interleave, with per-phase times and all-to-all bus bandwidth.
+The other configs are parity-test cases and --workload lines.
 
-Under torchrun (N > 1) every rank runs its own replica of the single-array
-workloads (cfg1-cfg3: the in-place path does not shard, "replicas only"),
-cfg4 shards the batch rows (no collective), and cfg5 runs the top-bit sharded
-plan with an NCCL all-to-all.  Rank 0 prints ONE JSON line.
+Timing: W untimed warm-up steps, then EXACTLY K steps, each bracketed by CUDA
+events on the stream the kernel is launched on, with a barrier + device
+synchronise on both sides; the per-rank time is the sum of the K step
+durations and the job time is the max over ranks.  Workloads whose working
+set is below 4x the L2 get an L2 flush (a 512 MiB write) before every step,
+outside the step's events; the others (cfg3: 32 GiB per step) exceed the L2
+by two orders of magnitude.
 
---impl reference times the reference's own CPU algorithm for the path (the C
-restatement in oracle/, parallel semi-recursive on all host threads; the
-reference itself is Python+numba and cannot travel to the GPU box) on rank 0.
+Under torchrun (N > 1) cfg1-cfg3 run one replica per rank ("replicas only":
+a single array does not shard without an exchange), cfg4 shards the batch
+rows (no collective), and cfg5 runs the top-bit sharded plan.  Rank 0 prints
+ONE JSON line.
+
+--impl reference times the reference's own CPU algorithm for the path on rank
+0 with all host threads: the C restatement in oracle/ (parallel
+semi-recursive, src/parallel.py:95-156) and, beside it, the reference package
+itself (baseline/_ref, numba) on the same sample; the line's value is the
+faster of the two.
 """
 
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -49,29 +61,35 @@ WORKLOADS = {
              "in-place bit reversal (tile-pair swap), n=2^26 float64"),
     "cfg3-4": (30, "float32", 4, False, 1, "out-of-place bit reversal, n=2^30 float32"),
     "cfg3-8": (30, "float64", 8, False, 1, "out-of-place bit reversal, n=2^30 float64"),
-    "cfg3-16": (30, "complex128", 16, False, 1, "out-of-place bit reversal, n=2^30 complex128"),
+    "cfg3-16": (30, "complex128", 16, False, 1,
+                "out-of-place bit reversal, n=2^30 complex128 (16 GiB per side; the largest "
+                "single-GPU BASELINE config)"),
     "cfg4": (16, "complex64", 8, False, 4096,
              "batched out-of-place bit reversal, 4096 x n=2^16 complex64 (FFT pre-pass)"),
     "cfg4-fft7": (16, "complex64", 8, False, 4096,
                   "batched FFT pre-pass, 4096 x n=2^16 complex64: bit reversal fused with the "
                   "first 7 radix-2 DIT stages"),
     "cfg5": (32, "complex64", 8, False, 1,
-             "n=2^32 complex64 sharded by top bits, local reversal + NCCL all-to-all + interleave"),
+             "n=2^32 complex64 sharded by top index bits: local reversal + NCCL "
+             "all_to_all_single + interleave"),
 }
 METRIC = "effective HBM GB/s (2*n*elem_bytes/time)"
 L2_BYTES = 126 * 10**6
 FALLBACK_HBM_GBS = 6650.0
+NVLINK_GBS_PER_DIRECTION = 900.0  # NVLink 5 through NVSwitch, per GPU per direction
 
 
 def parse():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: cfg3-16 on one GPU, cfg5 (sharded) on N > 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the cfg3 width sweep")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo + --same-device only to test the "
                          "multi-rank plumbing on one GPU)")
@@ -81,16 +99,20 @@ def parse():
                     help="override the library's tile bits Q for this workload (tuning)")
     ap.add_argument("--tile-path", type=int, default=-1,
                     help="override the staging path (0 register, 1 bulk ring, 2 tensor ring, "
-                         "3 rect [out of place], 4 cp.async / 5 TMA stores [in place])")
+                         "3 rect [out of place], 4 cp.async / 5 TMA stores / 6 cluster "
+                         "pairs [in place])")
     ap.add_argument("--chunks", type=int, default=4,
-                    help="cfg5: sub-chunks per all-to-all (exchange/unpack overlap)")
+                    help="cfg5: all-to-all rounds (round c+1 on the wire while c is interleaved)")
     ap.add_argument("--p2p", action="store_true",
                     help="cfg5: fused scatter into peer-mapped symmetric memory instead of NCCL")
     ap.add_argument("--no-soak", action="store_true",
                     help="skip the 0.5 s clock soak (for profiler runs)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0,
                     help="target seconds of CPU work for the cpu_baseline sample")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.workload is None:
+        args.workload = default_workload(dist_env()[0])
+    return args
 
 
 def dist_env():
@@ -98,6 +120,16 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def default_workload(world):
+    """N=1: the largest single-GPU config (the BASELINE metric names no single
+    config); N>1: the sharded single array, the config that scales across GPUs."""
+    return "cfg3-16" if world == 1 else "cfg5"
+
+
+def short_dtype(name):
+    return {"float32": "f32", "float64": "f64", "complex64": "c64", "complex128": "c128"}[name]
 
 
 # ---------------------------------------------------------------------------
@@ -196,89 +228,6 @@ class ClockSampler:
                 "samples": len(rows), "window": window}
 
 
-# ---------------------------------------------------------------------------
-# reference arm (CPU)
-
-
-def cpu_reference_step_fn(workload, threads):
-    """Return (step(), bytes_per_step, sample description, kind) running the
-    reference's CPU algorithm (C restatement, oracle/) on a host array."""
-    from oracle import oracle as orc
-
-    b, dtname, E, inplace, batch, _ = WORKLOADS[workload]
-    np_dt = {"float32": np.float32, "float64": np.float64, "complex64": np.complex64,
-             "complex128": np.complex128}[dtname]
-    rng = np.random.default_rng(0)
-    if workload.startswith("cfg4"):
-        # the reference has no batched API (and no FFT stages for cfg4-fft7:
-        # its CPU path is the permutation alone): rows over the threads (SURVEY 8(d) d8);
-        # each step permutes a bounded block of rows
-        rows = max(threads, 64)
-        arr = rng.standard_normal((rows, 1 << b)).astype(np_dt)
-
-        def step():
-            import concurrent.futures as cf
-
-            with cf.ThreadPoolExecutor(threads) as ex:
-                list(ex.map(lambda r: orc.c_cobra_inplace(arr[r], b, 6), range(rows)))
-
-        return step, 2 * rows * (1 << b) * E, f"{rows} of the 4096 rows per step", "port"
-    if workload == "cfg5":
-        b = 28  # bounded sample: 2^28 of the 2^32 elements per step
-    n = 1 << b
-    arr = rng.standard_normal(n).astype(np_dt) if np_dt in (np.float32, np.float64) else \
-        (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(np_dt)
-
-    def step():
-        orc.c_parallel_semi_recursive(arr, b, threads)
-
-    sample = f"full n=2^{b} array per step" if workload != "cfg5" else \
-        "n=2^28 of the 2^32-element array per step"
-    return step, 2 * n * E, sample, "port"
-
-
-def run_reference_arm(args):
-    world, rank, _ = dist_env()
-    if rank != 0:
-        return 0
-    from oracle import oracle as orc
-
-    orc.build()
-    threads = os.cpu_count() or 1
-    step, nbytes, sample, kind = cpu_reference_step_fn(args.workload, threads)
-    for _ in range(args.warmup):
-        step()
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        step()
-        ts.append(time.perf_counter() - t0)
-    total = sum(ts)
-    value = nbytes * len(ts) / total / 1e9
-    b, dtname, E, inplace, batch, desc = WORKLOADS[args.workload]
-    line = {
-        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(ts) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": short_dtype(dtname),
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.workload}: {desc}", "b": b, "elem_bytes": E,
-                   "inplace": inplace, "batch": batch},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
-                         "sample": sample,
-                         "method": "parallel_semi_recursive_permute (C port of src/parallel.py)"
-                         if not args.workload.startswith("cfg4")
-                         else "cobra_in_place per row on a thread pool"},
-        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0,
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-def short_dtype(name):
-    return {"float32": "f32", "float64": "f64", "complex64": "c64", "complex128": "c128"}[name]
-
-
 def host_info():
     info = {"logical_cpus": os.cpu_count()}
     try:
@@ -298,6 +247,149 @@ def host_info():
     return info
 
 
+# ---------------------------------------------------------------------------
+# the reference's CPU path (reference arm and cpu_baseline)
+
+
+def load_reference_package():
+    """The reference package itself, installed unmodified in baseline/_ref
+    (pip install --target), or None when absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "bitrev" / "__init__.py").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/bitrev_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import bitrev  # noqa: F401  (the reference, not this repo's package)
+
+        return bitrev
+    except Exception as exc:  # numba missing or broken: report, time the port alone
+        sys.stderr.write(f"reference package unavailable: {exc!r}\n")
+        return None
+
+
+NP_DTYPES = {"float32": np.float32, "float64": np.float64, "complex64": np.complex64,
+             "complex128": np.complex128}
+
+
+def _host_array(shape, np_dt):
+    """A host array with every page touched (its values do not matter to a
+    permutation's speed; a pattern fill is far cheaper than a random fill)."""
+    a = np.empty(shape, dtype=np_dt)
+    a.view(np.uint8).reshape(-1)[:] = 0x3F
+    return a
+
+
+def cpu_reference_runs(workload, threads):
+    """The reference's CPU algorithm for the workload's path, as a list of
+    (name, kind, step, bytes per step, sample, method): the C port (oracle/)
+    and, when baseline/_ref is present, the reference package itself.  Both
+    share one bounded host sample of the workload."""
+    from oracle import oracle as orc
+
+    orc.build()
+    b, dtname, E, inplace, batch, _ = WORKLOADS[workload]
+    np_dt = NP_DTYPES[dtname]
+    ref = load_reference_package()
+    runs = []
+    if workload.startswith("cfg4"):
+        # the reference has no batched API (and no FFT stages for cfg4-fft7:
+        # its CPU path is the permutation alone): rows over a thread pool
+        # created once (SURVEY 8(d) d8); each step permutes a bounded block of rows
+        import concurrent.futures as cf
+
+        rows = max(threads, 64)
+        arr = _host_array((rows, 1 << b), np_dt)
+        out = np.empty_like(arr)
+        pool = cf.ThreadPoolExecutor(threads)
+        sample = f"{rows} of the {batch} rows per step"
+
+        def port_step():
+            list(pool.map(lambda r: orc.c_cobra_inplace(arr[r], b, 6), range(rows)))
+
+        runs.append(("port", "port", port_step, 2 * rows * (1 << b) * E, sample,
+                     "cobra_in_place (C port of src/permutations.py:252-321) per row, "
+                     f"{threads}-thread pool"))
+        if ref is not None:
+            local = threading.local()
+
+            def row(r):
+                cfg = getattr(local, "cfg", None)
+                if cfg is None:
+                    cfg = local.cfg = ref.CobraConfig(6)
+                ref.cobra_out_of_place(arr[r], out[r], cfg, b)
+
+            def ref_step():
+                list(pool.map(row, range(rows)))
+
+            runs.append(("reference", "reference", ref_step, 2 * rows * (1 << b) * E, sample,
+                         "bitrev.cobra_out_of_place (baseline/_ref, numba) per row, "
+                         f"{threads}-thread pool"))
+        return runs
+    if workload == "cfg5":
+        b = 28  # bounded sample: 2^28 of the 2^32 elements per step
+    n = 1 << b
+    arr = _host_array(n, np_dt)
+    sample = (f"full n=2^{b} array per step" if workload != "cfg5" else
+              "n=2^28 of the 2^32-element array per step")
+
+    def port_step():
+        orc.c_parallel_semi_recursive(arr, b, threads)
+
+    runs.append(("port", "port", port_step, 2 * n * E, sample,
+                 f"parallel_semi_recursive_permute (C port of src/parallel.py:95-156), "
+                 f"{threads} threads"))
+    if ref is not None:
+        pcfg = ref.ParallelConfig(threads=threads)
+
+        def ref_step():
+            ref.parallel_semi_recursive_permute(arr, b, pcfg)
+
+        runs.append(("reference", "reference", ref_step, 2 * n * E, sample,
+                     f"bitrev.parallel_semi_recursive_permute (baseline/_ref, numba), "
+                     f"{threads} threads"))
+    return runs
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    runs = cpu_reference_runs(args.workload, threads)
+    results = {}
+    for name, kind, step, nbytes, sample, method in runs:
+        for _ in range(max(args.warmup, 1)):  # the first call also JIT-compiles numba
+            step()
+        ts = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            step()
+            ts.append(time.perf_counter() - t0)
+        results[name] = {"value": nbytes * len(ts) / sum(ts) / 1e9, "unit": "GB/s",
+                         "kind": kind, "ms_per_step": sum(ts) / len(ts) * 1e3,
+                         "sample": sample, "method": method}
+    best = max(results.values(), key=lambda r: r["value"])
+    value = best["value"]
+    b, dtname, E, inplace, batch, desc = WORKLOADS[args.workload]
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": best["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": short_dtype(dtname), "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.workload}: {desc}", "b": b, "elem_bytes": E,
+                   "inplace": inplace, "batch": batch},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": best["kind"],
+                         "sample": best["sample"], "method": best["method"],
+                         "runs": results, "host": host_info()},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def single_thread_methods(workload, budget_s=20.0):
     """The reference's single-thread methods on the same array:
     COBRA (q = default_cobra_q), semi-recursive and recursive, once each, GB/s."""
@@ -306,10 +398,7 @@ def single_thread_methods(workload, budget_s=20.0):
     b, dtname, E, inplace, batch, _ = WORKLOADS[workload]
     if workload.startswith("cfg4") or workload == "cfg5" or (1 << b) * E > (2 << 30):
         return None
-    np_dt = {"float32": np.float32, "float64": np.float64, "complex64": np.complex64,
-             "complex128": np.complex128}[dtname]
-    a = np.empty(1 << b, dtype=np_dt)
-    a.fill(1)  # touch every page before timing
+    a = _host_array(1 << b, NP_DTYPES[dtname])
     q = min(b // 2, 6)
     runs = [("cobra_in_place" if inplace else "cobra_out_of_place",
              (lambda: orc.c_cobra_inplace(a, b, q)) if inplace else (lambda: orc.c_cobra_oop(a, b, q))),
@@ -323,32 +412,278 @@ def single_thread_methods(workload, budget_s=20.0):
         t0 = time.perf_counter()
         fn()
         out[name] = round(2 * a.nbytes / (time.perf_counter() - t0) / 1e9, 3)
-    return {"unit": "GB/s", "threads": 1, "values": out}
+    return {"unit": "GB/s", "threads": 1, "values": out, "kind": "port"}
 
 
 def cpu_baseline(workload, target_s):
-    """The C port timed on the host cores, bounded to ~target_s of CPU work."""
+    """The reference's CPU path timed on the host cores (the C port and the
+    reference package itself), each bounded to ~target_s of CPU work."""
     threads = os.cpu_count() or 1
-    step, nbytes, sample, kind = cpu_reference_step_fn(workload, threads)
-    step()  # warm (page faults, thread start-up)
-    ts = []
-    t_start = time.perf_counter()
-    while True:
+    runs = cpu_reference_runs(workload, threads)
+    results = {}
+    for name, kind, step, nbytes, sample, method in runs:
         t0 = time.perf_counter()
-        step()
-        ts.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start > target_s / threads or len(ts) >= 50:
-            break
-    total = sum(ts)
-    return {"value": nbytes * len(ts) / total / 1e9, "unit": "GB/s", "cores": threads,
-            "kind": kind, "sample": f"{sample}, {len(ts)} steps",
-            "method": "parallel_semi_recursive_permute (C port of src/parallel.py:95-156)"
-            if not workload.startswith("cfg4") else "cobra_in_place per row on a thread pool",
+        step()  # warm (page faults, thread start-up, numba JIT)
+        if time.perf_counter() - t0 < 2.0:  # first touches of a fresh sample run slow
+            step()
+            step()
+        ts = []
+        t_start = time.perf_counter()
+        while True:
+            t0 = time.perf_counter()
+            step()
+            ts.append(time.perf_counter() - t0)
+            if time.perf_counter() - t_start > target_s / threads or len(ts) >= 50:
+                break
+        results[name] = {"value": nbytes * len(ts) / sum(ts) / 1e9, "unit": "GB/s", "kind": kind,
+                         "sample": f"{sample}, {len(ts)} steps", "method": method}
+    best = max(results.values(), key=lambda r: r["value"])
+    del runs
+    gc.collect()
+    return {"value": best["value"], "unit": "GB/s", "cores": threads, "kind": best["kind"],
+            "sample": best["sample"], "method": best["method"], "runs": results,
             "host": host_info(), "single_thread": single_thread_methods(workload)}
 
 
 # ---------------------------------------------------------------------------
 # our arm
+
+
+class Flush:
+    """Write a 512 MiB buffer (evicts the inputs from the 126 MB L2), then read
+    a 256 MiB one so the L2 is left holding clean lines: otherwise the timed
+    kernel would pay for writing back the flush's own dirty lines."""
+
+    def __init__(self, torch, dev):
+        self.torch = torch
+        self.w = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        self.r = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
+        self.sink = torch.empty((), dtype=torch.float32, device=dev)
+
+    def zero_(self):
+        self.w.zero_()
+        self.torch.sum(self.r, dim=0, out=self.sink)
+
+
+def time_steps(torch, step, steps, stream, flush=None):
+    """Per-step seconds of `steps` steps, each bracketed by CUDA events on
+    `stream` (flush, if any, outside the events)."""
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for k in range(steps):
+        if flush is not None:
+            flush.zero_()
+        starts[k].record(stream)
+        step()
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
+
+
+def width_sweep(torch, dev, peak, steps):
+    """cfg3-4 and cfg3-8 (config 3's element-width sweep) on the same device,
+    same protocol (inputs far larger than the L2, no flush), fewer steps."""
+    from paper_1708_01873_b200 import _core, _lib
+
+    out = {}
+    stream = torch.cuda.current_stream(dev)
+    for w in ("cfg3-4", "cfg3-8"):
+        b, dtname, E, _, _, desc = WORKLOADS[w]
+        x = torch.empty((1 << b) * E, dtype=torch.uint8, device=dev).random_(0, 256)
+        x = x.view(getattr(torch, dtname))
+        y = torch.empty_like(x)
+
+        def step():
+            _core.launch_oop(x, y, b)
+
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        ts = time_steps(torch, step, steps, stream)
+        nbytes = 2 * (1 << b) * E
+        v = nbytes * len(ts) / sum(ts) / 1e9
+        q, path = _lib.last_tile()
+        out[w] = {"value": v, "unit": "GB/s", "gelem_per_s": v / (2 * E), "frac": v / peak,
+                  "ms_per_step": sum(ts) / len(ts) * 1e3, "steps": steps, "tile_bits": q,
+                  "tile_path": path, "workload": desc}
+        del x, y
+        torch.cuda.empty_cache()
+    return out
+
+
+def e2e_host(torch, br, x, b, E, inplace, workload, steps, stream):
+    """End to end through the public API with host buffers (rank 0's replica).
+
+    e2e: bitrev_host_pipeline over a stream of pinned host arrays (each step =
+    one array: its H2D copy, the permutation and its D2H copy; consecutive
+    steps overlap their copies in opposite directions).  e2e_single: one
+    blocking reference-style call per array (cobra_in_place /
+    cobra_out_of_place / bitrev_batched / bitrev_dit_prepass on a host tensor:
+    H2D, kernel, D2H, sync, nothing overlapped).  All host buffers are freed
+    before returning."""
+    n_local = x.numel()
+    bytes_local = 2 * n_local * E
+    nhost = 3
+    hosts = [x.cpu().pin_memory() for _ in range(nhost)]
+    houts = None if inplace else [torch.empty_like(h).pin_memory() for h in hosts]
+    cfg = br.CobraConfig(6)
+    reps = max(3, min(steps, 32))
+    e2e = e2e_single = None
+
+    def run_pipeline():
+        srcs = [hosts[k % nhost] for k in range(reps)]
+        dsts = None if houts is None else [houts[k % nhost] for k in range(reps)]
+        br.bitrev_host_pipeline(srcs, b, dsts)
+
+    def single_step():
+        if workload == "cfg4-fft7":
+            br.bitrev_dit_prepass(hosts[0], b, 7, out=houts[0])
+        elif workload == "cfg4":
+            br.bitrev_batched(hosts[0], b, houts[0])
+        elif inplace:
+            br.cobra_in_place(hosts[0], cfg, b)
+        else:
+            br.cobra_out_of_place(hosts[0], houts[0], cfg, b)
+
+    plan = ((run_pipeline, reps, "pipe"), (single_step, 1, "single"))
+    if workload == "cfg4-fft7":  # the host pipeline runs the plain permutation
+        plan = ((single_step, 1, "single"),)
+    for fn, n_steps, key in plan:
+        fn()  # warm (stream/pool creation, page-locking caches)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        loops = 1 if key == "pipe" else min(reps, 5)
+        ev0.record(stream)
+        for _ in range(loops):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        t_step = ev0.elapsed_time(ev1) / 1e3 / (n_steps * loops)
+        rec = {"value": bytes_local / t_step / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": n_local * E, "d2h_bytes_per_step": n_local * E,
+               "ms_per_step": t_step * 1e3}
+        if key == "pipe":
+            rec["path"] = (f"bitrev_host_pipeline over {reps} pinned host arrays (public API; "
+                           "per step: H2D + permute + D2H, consecutive steps overlapped)")
+            e2e = rec
+        else:
+            rec["path"] = ("one blocking call per array on a pinned host tensor "
+                           "(cobra_in_place / cobra_out_of_place / bitrev_batched / "
+                           "bitrev_dit_prepass)")
+            e2e_single = rec
+    if e2e is None:
+        e2e = e2e_single
+    else:
+        # PCIe ceiling for the pipeline, same harness: each step one H2D and one
+        # D2H of the step's bytes on two streams, nothing else (no kernel).
+        d_in, d_out = torch.empty_like(x), torch.empty_like(x)
+        h_out = houts if houts is not None else hosts
+        s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
+        for timed in (False, True):
+            torch.cuda.synchronize()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            s_up.wait_stream(stream)
+            s_down.wait_stream(stream)
+            for k in range(reps if timed else 2):
+                with torch.cuda.stream(s_up):
+                    d_in.copy_(hosts[k % nhost], non_blocking=True)
+                with torch.cuda.stream(s_down):
+                    h_out[(k + 1) % nhost].copy_(d_out, non_blocking=True)
+            stream.wait_stream(s_up)
+            stream.wait_stream(s_down)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        ceil = bytes_local / (ev0.elapsed_time(ev1) / 1e3 / reps) / 1e9
+        e2e["pcie_ceiling_gbs"] = ceil
+        e2e["frac_of_pcie_ceiling"] = e2e["value"] / ceil
+        e2e["pcie_ceiling_path"] = ("concurrent pinned H2D + D2H of the step's bytes on two "
+                                    "streams, no kernel (same harness)")
+        del d_in, d_out
+    del hosts, houts
+    gc.collect()
+    torch.cuda.empty_cache()
+    return e2e, e2e_single
+
+
+def e2e_sharded(torch, dist, sharded, x, b, chunks, steps, stream, world):
+    """cfg5 end to end through sharded_bitrev: every rank copies its shard in
+    from pinned host memory, runs the sharded permutation, and copies its
+    output shard back; max over ranks."""
+    E = x.element_size()
+    host_in = x.cpu().pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    dev_in = torch.empty_like(x)
+
+    def step():
+        dev_in.copy_(host_in, non_blocking=True)
+        out = sharded.sharded_bitrev(dev_in, b, chunks=chunks)
+        host_out.copy_(out, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    reps = max(3, min(steps, 5))
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(reps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([ev0.elapsed_time(ev1) / 1e3 / reps], dtype=torch.float64, device=x.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t.item())
+    rec = {"value": (1 << b) * 2 * E / t_step / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": x.numel() * E, "d2h_bytes_per_step": x.numel() * E,
+           "bytes_are": "per rank (each rank moves its own shard)", "ms_per_step": t_step * 1e3,
+           "path": "per rank: pinned H2D of the shard, sharded_bitrev (pack, all_to_all_single "
+                   "rounds, unpack), D2H of the output shard; max over ranks"}
+    del host_in, host_out, dev_in
+    gc.collect()
+    torch.cuda.empty_cache()
+    return rec
+
+
+def cfg5_phases(torch, dist, sharded, x, b, world, reps=3):
+    """Per-phase device times of the sharded plan with one exchange round
+    (pack -> all_to_all_single -> unpack), median of `reps`, max over ranks."""
+    names = ("pack", "a2a", "unpack")
+    acc = {k: [] for k in names}
+    for _ in range(reps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ph = {}
+        sharded.sharded_bitrev(x, b, chunks=1, phases=ph)
+        torch.cuda.synchronize()
+        acc["pack"].append(ph["t0"].elapsed_time(ph["packed"]) / 1e3)
+        acc["a2a"].append(ph["packed"].elapsed_time(ph["exchanged"]) / 1e3)
+        acc["unpack"].append(ph["exchanged"].elapsed_time(ph["done"]) / 1e3)
+    med = torch.tensor([statistics.median(acc[k]) for k in names], dtype=torch.float64,
+                       device=x.device)
+    if world > 1:
+        dist.all_reduce(med, op=dist.ReduceOp.MAX)
+    t = dict(zip(names, med.tolist()))
+    S = x.numel() * x.element_size()  # per-rank shard bytes
+    out = {"ms": {k: v * 1e3 for k, v in t.items()}, "shard_bytes": S,
+           "method": f"CUDA events on the current stream, one round, median of {reps}, max over ranks"}
+    if world > 1 and t["a2a"] > 0:
+        algbw = S / t["a2a"] / 1e9
+        busbw = algbw * (world - 1) / world
+        out["a2a"] = {"algbw_gbs": algbw, "busbw_gbs": busbw,
+                      "peak_gbs_per_direction": NVLINK_GBS_PER_DIRECTION,
+                      "frac_of_nvlink": busbw / NVLINK_GBS_PER_DIRECTION,
+                      "convention": "nccl-tests: algbw = shard bytes / time, "
+                                    "busbw = algbw * (G-1)/G"}
+    if t["pack"] > 0:
+        out["pack_hbm_gbs"] = 2 * S / t["pack"] / 1e9
+    if t["unpack"] > 0 and world > 1:
+        out["unpack_hbm_gbs"] = 2 * S / t["unpack"] / 1e9
+    return out
 
 
 def main():
@@ -367,12 +702,16 @@ def main():
         dev_index = 0 if args.same_device else local
         torch.cuda.set_device(dev_index)
         if args.dist_backend == "nccl":
+            # NCCL's init lines (rank / nranks / transport) go to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
         else:
             dist.init_process_group("gloo")
     dev = torch.device("cuda", torch.cuda.current_device())
     b, dtname, E, inplace, batch, desc = WORKLOADS[args.workload]
     dtype = getattr(torch, dtname)
+    peak, peak_src = load_peak()
 
     # per-rank work
     if args.workload.startswith("cfg4"):
@@ -380,9 +719,6 @@ def main():
         scaling = "strong"
         shape = (rows, 1 << b)
     elif args.workload == "cfg5":
-        if world < 2:
-            sys.stderr.write("cfg5 needs --gpus >= 2 (torchrun)\n")
-            return 2
         g = sharded.check_plan(b, world)
         shape = (1 << (b - g),)
         scaling = "strong"
@@ -394,27 +730,31 @@ def main():
 
     x = torch.empty(n_local * E, dtype=torch.uint8, device=dev).random_(0, 256).view(dtype)
     x = x.view(shape)
-    y = None if inplace else torch.empty_like(x)
+    y = None if (inplace or args.workload == "cfg5") else torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
 
     if args.tile_bits:
         _lib.set_tile_bits(E, inplace, args.tile_bits)
     if args.tile_path >= 0:
         _lib.set_tile_path(E, inplace, args.tile_path)
-    exchange = "nccl all_to_all"
-    if args.workload == "cfg5" and args.p2p:
-        try:
-            peers, p2p_barrier, _keep = sharded.symmetric_recv(n_local, dtype, dev)
-            exchange = "fused scatter into symmetric memory (NVLink peer stores)"
+    exchange = None
+    if args.workload == "cfg5":
+        exchange = (f"NCCL all_to_all_single in {args.chunks} rounds, round c interleaved while "
+                    "c+1.. are on the wire" if world > 1 else "none (one GPU holds the array)")
+        chunks = args.chunks if world > 1 else 1
+        if args.p2p and world > 1:
+            try:
+                peers, p2p_barrier, _keep = sharded.symmetric_recv(n_local, dtype, dev)
+                exchange = "fused scatter into symmetric memory (NVLink peer stores)"
 
+                def step():
+                    return sharded.sharded_bitrev_p2p(x, b, peers, rank, p2p_barrier)
+            except Exception as exc:  # no peer mapping available: report and use NCCL
+                exchange = f"{exchange} (p2p unavailable: {type(exc).__name__})"
+                args.p2p = False
+        if not (args.p2p and world > 1):
             def step():
-                return sharded.sharded_bitrev_p2p(x, b, peers, rank, p2p_barrier)
-        except Exception as exc:  # no peer mapping available: report and use NCCL
-            exchange = f"nccl all_to_all (p2p unavailable: {type(exc).__name__})"
-            args.p2p = False
-    if args.workload == "cfg5" and not args.p2p:
-        def step():
-            return sharded.sharded_bitrev(x, b, chunks=args.chunks)
+                return sharded.sharded_bitrev(x, b, chunks=chunks)
     elif args.workload == "cfg4-fft7":
         n_rows = shape[0]
 
@@ -429,22 +769,7 @@ def main():
             _core.launch_oop(x, y, b)
 
     need_flush = 2 * bytes_local < 4 * L2_BYTES and args.workload != "cfg5"
-
-    class _Flush:
-        """Write a 512 MiB buffer (evicts the inputs from the 126 MB L2), then
-        read a 256 MiB one so the L2 is left holding clean lines: otherwise the
-        timed kernel would pay for writing back the flush's own dirty lines."""
-
-        def __init__(self):
-            self.w = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-            self.r = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
-            self.sink = torch.empty((), dtype=torch.float32, device=dev)
-
-        def zero_(self):
-            self.w.zero_()
-            torch.sum(self.r, dim=0, out=self.sink)
-
-    flush = _Flush() if need_flush else None
+    flush = Flush(torch, dev) if need_flush else None
 
     sampler = ClockSampler(dev.index)
     sampler.start()
@@ -463,26 +788,17 @@ def main():
             step()
         torch.cuda.synchronize()
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     t_wall0 = time.monotonic()
-    for k in range(args.steps):
-        if flush is not None:
-            flush.zero_()
-        starts[k].record(stream)
-        step()
-        ends[k].record(stream)
-    torch.cuda.synchronize()
+    step_s = time_steps(torch, step, args.steps, stream, flush)
     t_wall1 = time.monotonic()
     launches = _lib.launch_count() - launches0
     chosen = _lib.last_tile()  # (tile bits, staging path) the timed launches used
     if world > 1:
         dist.barrier()
-    step_s = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
     rank_time = sum(step_s)
     if world > 1:
         t = torch.tensor([rank_time], dtype=torch.float64,
@@ -492,6 +808,11 @@ def main():
     else:
         job_time = rank_time
     sampler.mark("load1")
+
+    # cfg5: per-phase times and all-to-all bandwidth (one round, instrumented)
+    phases = None
+    if args.workload == "cfg5" and not args.p2p:
+        phases = cfg5_phases(torch, dist, sharded, x, b, world)
 
     # same-harness reference: torch copy_ of the same bytes with the same
     # flush protocol (a device copy moves 2*n*E bytes, like one permutation)
@@ -546,93 +867,21 @@ def main():
                             "no L2 flush (working set L2-resident)"}
         del graph
 
-    # end-to-end through the public API with host buffers (rank 0's replica).
-    # e2e: bitrev_host_pipeline over a stream of host arrays (each step = one
-    # array: its H2D copy, the permutation and its D2H copy; consecutive steps
-    # overlap their copies in opposite directions).  e2e_single: one blocking
-    # reference-style call per array (cobra_in_place / cobra_out_of_place on
-    # a host tensor: H2D, kernel, D2H, sync, nothing overlapped).
-    e2e = None
-    e2e_single = None
-    if not args.no_e2e and args.workload != "cfg5":
-        nhost = 3
-        hosts = [x.cpu().pin_memory() for _ in range(nhost)]
-        houts = None if inplace else [torch.empty_like(h).pin_memory() for h in hosts]
-        cfg = br.CobraConfig(6)
-        reps = max(3, min(args.steps, 32))
-
-        def run_pipeline():
-            srcs = [hosts[k % nhost] for k in range(reps)]
-            dsts = None if houts is None else [houts[k % nhost] for k in range(reps)]
-            br.bitrev_host_pipeline(srcs, b, dsts)
-
-        def single_step():
-            if args.workload == "cfg4-fft7":
-                br.bitrev_dit_prepass(hosts[0], b, 7, out=houts[0])
-            elif args.workload == "cfg4":
-                br.bitrev_batched(hosts[0], b, houts[0])
-            elif inplace:
-                br.cobra_in_place(hosts[0], cfg, b)
-            else:
-                br.cobra_out_of_place(hosts[0], houts[0], cfg, b)
-
-        plan = ((run_pipeline, reps, "pipe"), (single_step, 1, "single"))
-        if args.workload == "cfg4-fft7":  # the host pipeline runs the plain permutation
-            plan = ((single_step, 1, "single"),)
-        for fn, n_steps, key in plan:
-            fn()  # warm (stream/pool creation, page-locking caches)
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            loops = 1 if key == "pipe" else reps
-            ev0.record(stream)
-            for _ in range(loops):
-                fn()
-            ev1.record(stream)
-            torch.cuda.synchronize()
-            t_step = ev0.elapsed_time(ev1) / 1e3 / (n_steps * loops)
-            rec = {"value": bytes_local / t_step / 1e9, "unit": "GB/s",
-                   "h2d_bytes_per_step": n_local * E, "d2h_bytes_per_step": n_local * E,
-                   "ms_per_step": t_step * 1e3}
-            if key == "pipe":
-                rec["path"] = (f"bitrev_host_pipeline over {reps} pinned host arrays (public API; "
-                               "per step: H2D + permute + D2H, consecutive steps overlapped)")
-                e2e = rec
-            else:
-                rec["path"] = ("one blocking call per array on a pinned host tensor "
-                               "(cobra_in_place / cobra_out_of_place / bitrev_batched / "
-                               "bitrev_dit_prepass)")
-                e2e_single = rec
-        if e2e is None:
-            e2e = e2e_single
-        else:
-            # PCIe ceiling for the pipeline, same harness: each step one H2D and one
-            # D2H of the step's bytes on two streams, nothing else (no kernel).
-            d_in, d_out = torch.empty_like(x), torch.empty_like(x)
-            h_out = houts if houts is not None else hosts
-            s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
-            for timed in (False, True):
-                torch.cuda.synchronize()
-                ev0 = torch.cuda.Event(enable_timing=True)
-                ev1 = torch.cuda.Event(enable_timing=True)
-                ev0.record(stream)
-                s_up.wait_stream(stream)
-                s_down.wait_stream(stream)
-                for k in range(reps if timed else 2):
-                    with torch.cuda.stream(s_up):
-                        d_in.copy_(hosts[k % nhost], non_blocking=True)
-                    with torch.cuda.stream(s_down):
-                        h_out[(k + 1) % nhost].copy_(d_out, non_blocking=True)
-                stream.wait_stream(s_up)
-                stream.wait_stream(s_down)
-                ev1.record(stream)
-                torch.cuda.synchronize()
-            ceil = bytes_local / (ev0.elapsed_time(ev1) / 1e3 / reps) / 1e9
-            e2e["pcie_ceiling_gbs"] = ceil
-            e2e["frac_of_pcie_ceiling"] = e2e["value"] / ceil
-            e2e["pcie_ceiling_path"] = ("concurrent pinned H2D + D2H of the step's bytes on two "
-                                        "streams, no kernel (same harness)")
-            del d_in, d_out
+    e2e = e2e_single = None
+    if not args.no_e2e:
+        if args.workload == "cfg5":
+            if world > 1 and not args.p2p:
+                e2e = e2e_sharded(torch, dist, sharded, x, b, args.chunks, args.steps, stream, world)
+        elif rank == 0:
+            e2e, e2e_single = e2e_host(torch, br, x, b, E, inplace, args.workload, args.steps,
+                                       stream)
+    sweep = None
+    if args.workload == "cfg3-16" and not args.no_sweep:
+        del x, y
+        x = y = None
+        gc.collect()
+        torch.cuda.empty_cache()
+        sweep = width_sweep(torch, dev, peak, max(5, min(args.steps, 10)))
     sampler.stop()
     clocks = sampler.summary(t_wall0, t_wall1)
 
@@ -642,13 +891,14 @@ def main():
         dist.destroy_process_group()
         return 0
 
-    peak, peak_src = load_peak()
     avg_launch = statistics.mean(step_s)
     achieved = bytes_local / avg_launch / 1e9
     value = world * bytes_local * args.steps / job_time / 1e9
     if args.workload == "cfg5":
         value = (1 << b) * 2 * E * args.steps / job_time / 1e9
     traffic = load_traffic(args.workload)
+    kernel = ("bitrev_fft_rect_kernel" if args.workload == "cfg4-fft7" else
+              "bitrev_inplace_tile_kernel" if inplace else "bitrev oop tile kernel")
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": job_time / args.steps * 1e3,
@@ -663,15 +913,14 @@ def main():
                             }.get(args.workload, f"replicas only ({world} independent arrays)"),
             "l2": "L2 flushed before every step (512 MiB write, then a 256 MiB read so "
                   "no dirty flush lines remain), outside the step's events" if need_flush else
-                  f"working set {bytes_local // 2 >> 20} MiB per side > L2, no flush",
+                  f"inputs larger than L2 ({bytes_local // 2 >> 20} MiB per side per rank), "
+                  "no flush",
             "tile_bits": None if args.workload == "cfg4-fft7" else chosen[0],
             "tile_path": None if args.workload == "cfg4-fft7" else chosen[1],
         },
         "gelem_per_s": value / (2 * E),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("bitrev_fft_rect_kernel" if args.workload == "cfg4-fft7" else
-                                "bitrev_inplace_tile_kernel" if inplace else "bitrev oop tile kernel"),
+                     "frac": achieved / peak, "traffic": traffic, "kernel": kernel,
                      "algorithmic_bytes_per_launch": bytes_local, "peak_source": peak_src,
                      "frac_of_8TBs_spec": achieved / 8000.0,
                      "torch_copy_same_harness_gbs": copy_ref,
@@ -684,9 +933,22 @@ def main():
         "step_ms": {"median": statistics.median(step_s) * 1e3, "min": min(step_s) * 1e3,
                     "max": max(step_s) * 1e3},
     }
+    if sweep is not None:
+        line["width_sweep"] = sweep
     if args.workload == "cfg5":
-        line["roofline"]["kernel"] = f"local bitrev + {exchange} + unpack"
         line["config"]["exchange"] = exchange
+        line["config"]["chunks"] = args.chunks if world > 1 else 1
+        if world > 1:
+            # the step is NVLink-bound; the HBM roofline applies to the local passes
+            line["roofline"]["kernel"] = "local pack (bitrev_sharded_pack) + unpack"
+            line["roofline"]["achieved_note"] = ("per-rank step bytes 2*S / step time "
+                                                 "(all three phases)")
+            if phases and "a2a" in phases:
+                line["nvlink_roofline"] = phases["a2a"]
+        else:
+            line["roofline"]["kernel"] = "bitrev oop tile kernel (2^32 elements on one GPU)"
+        if phases is not None:
+            line["phases"] = phases
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args.workload, args.cpu_sample_s)

@@ -169,6 +169,19 @@ int bitrev_sharded_scatter(const void* local, void* const* peer_recv, int b_loca
                            int elem_bytes, void* stream);
 
 /*
+ * Step 1 of the top-bit sharded plan for an all-to-all in 2^chunk_bits
+ * rounds (no reference counterpart): the local reversal of
+ * the 2^b_local-element shard written to `send` in the layout
+ * [sub-chunk c][destination d][k'], sub-chunk length S = 2^(b_local-g-chunk_bits),
+ * for local output index u = d*C + c*S + k'.  Row c of `send` (G*S elements)
+ * is then the equal-split input of one all-to-all round.  chunk_bits = 0 is
+ * exactly bitrev_oop.  Requires b_local >= 2g + chunk_bits, G <= 8, and (for
+ * chunk_bits > 0) S >= the scatter tile side (64 / 32 / 32 for 4 / 8 / 16 B).
+ */
+int bitrev_sharded_pack(const void* local, void* send, int b_local, int g, int chunk_bits,
+                        int elem_bytes, void* stream);
+
+/*
  * Step 3 of the top-bit sharded plan (no reference counterpart: the reference
  * has no multi-device path).  recv holds G = 2^g
  * chunks of C = 2^(b_local-g) elements, chunk r received from rank r;

@@ -34,6 +34,7 @@ SIGNATURES = {
     "bitrev_dit_prepass": (_c_int, [_vp, _vp, _c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_int,
                                     _c_int, _vp]),
     "bitrev_sharded_scatter": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "bitrev_sharded_pack": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "bitrev_sharded_unpack": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _vp]),
     "bitrev_get_tile_bits": (_c_int, [_c_int, _c_int]),
     "bitrev_set_tile_bits": (_c_int, [_c_int, _c_int, _c_int]),

@@ -802,6 +802,43 @@ int note(int rc, int q, int path) {
   return rc;
 }
 
+
+// Steps 1(+2) of the sharded plan: the local (b_local)-bit reversal with each
+// destination row stored at peer[d] + ((c << (sb + g)) | (rank << sb) | k') * E
+// for local output index u = d * C + c * 2^sb + k'.
+int launch_scatter(const void* local, char* const* peer, int b_local, int g, int rank, int sb,
+                   int E, cudaStream_t st) {
+  const int q = E == 4 ? 6 : 5;  // 256 / 256 / 512-byte rows
+  if (sb < q || 2 * q > b_local) return BITREV_ESHARD;  // rows inside one sub-chunk
+  if (!aligned16(local)) return BITREV_EALIGN;
+  ScatterArgs sa;
+  memset(&sa, 0, sizeof sa);
+  for (int d = 0; d < (1 << g); ++d) {
+    if (!peer[d] || !aligned16(peer[d])) return BITREV_ENULL;
+    sa.peer[d] = peer[d];
+  }
+  sa.g = g;
+  sa.rank = rank;
+  sa.sb = sb;
+  TileArgs& a = sa.t;
+  a.src = static_cast<const char*>(local);
+  a.b = b_local;
+  a.m = b_local - 2 * q;
+  a.ntiles = 1ull << a.m;
+  a.batch = 1;
+#define SCATTER(E_, Q_)                                                                   \
+  if (E == E_ && q == Q_) {                                                               \
+    using T = Tile<E_, Q_>;                                                               \
+    auto kern = bitrev_scatter_tile_kernel<E_, Q_>;                                       \
+    const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);                        \
+    kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(sa);                   \
+    return finish_launch();                                                               \
+  }
+  SCATTER(4, 6) SCATTER(8, 5) SCATTER(16, 5)
+#undef SCATTER
+  return BITREV_ETILE;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1277,35 +1314,30 @@ int bitrev_sharded_scatter(const void* local, void* const* peer_recv, int b_loca
   if (E != 4 && E != 8 && E != 16) return BITREV_EELEM;
   if (g < 0 || (1 << g) > kMaxPeers || rank < 0 || rank >= (1 << g)) return BITREV_ESHARD;
   if (!local || !peer_recv) return BITREV_ENULL;
-  const int q = E == 4 ? 6 : 5;  // 256 / 256 / 512-byte rows
-  if (b_local - g < q || 2 * q > b_local) return BITREV_ESHARD;  // rows inside one chunk
-  ScatterArgs sa;
-  memset(&sa, 0, sizeof sa);
-  for (int d = 0; d < (1 << g); ++d) {
-    if (!peer_recv[d] || !aligned16(peer_recv[d])) return BITREV_ENULL;
-    sa.peer[d] = static_cast<char*>(peer_recv[d]);
-  }
-  if (!aligned16(local)) return BITREV_EALIGN;
-  sa.g = g;
-  sa.rank = rank;
-  TileArgs& a = sa.t;
-  a.src = static_cast<const char*>(local);
-  a.b = b_local;
-  a.m = b_local - 2 * q;
-  a.ntiles = 1ull << a.m;
-  a.batch = 1;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define SCATTER(E_, Q_)                                                                   \
-  if (E == E_ && q == Q_) {                                                               \
-    using T = Tile<E_, Q_>;                                                               \
-    auto kern = bitrev_scatter_tile_kernel<E_, Q_>;                                       \
-    const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);                        \
-    kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(sa);                   \
-    return finish_launch();                                                               \
-  }
-  SCATTER(4, 6) SCATTER(8, 5) SCATTER(16, 5)
-#undef SCATTER
-  return BITREV_ETILE;
+  if (b_local < 2 * g) return BITREV_ESHARD;
+  char* peer[kMaxPeers] = {};
+  for (int d = 0; d < (1 << g); ++d) peer[d] = static_cast<char*>(peer_recv[d]);
+  return launch_scatter(local, peer, b_local, g, rank, b_local - g, E,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int bitrev_sharded_pack(const void* local, void* send, int b_local, int g, int chunk_bits,
+                        int elem_bytes, void* stream) {
+  const int E = elem_bytes;
+  if (b_local < 1 || b_local > kMaxBits) return BITREV_EWIDTH;
+  if (E != 4 && E != 8 && E != 16) return BITREV_EELEM;
+  if (g < 0 || (1 << g) > kMaxPeers || chunk_bits < 0 || b_local < 2 * g + chunk_bits)
+    return BITREV_ESHARD;
+  if (!local || !send) return BITREV_ENULL;
+  const uintptr_t l0 = (uintptr_t)local, s0 = (uintptr_t)send;
+  const uintptr_t bytes = (uintptr_t)E << b_local;
+  if (l0 < s0 + bytes && s0 < l0 + bytes) return BITREV_EOVERLAP;
+  if (chunk_bits == 0)  // one chunk: the send layout is the plain reversal
+    return bitrev_oop(local, send, b_local, E, 1, 0, 0, stream);
+  const int sb = b_local - g - chunk_bits;
+  char* peer[kMaxPeers] = {};
+  for (int d = 0; d < (1 << g); ++d) peer[d] = static_cast<char*>(send) + ((uint64_t)E << sb) * d;
+  return launch_scatter(local, peer, b_local, g, 0, sb, E, static_cast<cudaStream_t>(stream));
 }
 
 int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int elem_bytes,
@@ -1317,25 +1349,35 @@ int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int e
   if (!recv || !dst) return BITREV_ENULL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t C = 1ull << (b_local - g);
-  const unsigned grid = (unsigned)elementwise_grid(C);
   const char* r = static_cast<const char*>(recv);
   char* d = static_cast<char*>(dst);
-#define UNPACK_G(E_, G_)                                            \
-  case G_:                                                          \
-    sharded_unpack_kernel<E_, G_><<<grid, 256, 0, st>>>(r, d, C);   \
+  // vector kernel: 16-byte aligned, at least 16 bytes per source chunk, G <= 8
+  const bool vec = aligned16(recv) && aligned16(dst) && C * (uint64_t)E >= 16 && g <= 3 &&
+                   (E == 4 || E == 8 || E == 16);
+  if (vec) {
+    const uint64_t threads = C / (16 / E);
+    const unsigned grid = (unsigned)grid_for((threads + 255) / 256, 8);
+#define UNPACK_G(E_, G_)                                                  \
+  case G_:                                                                \
+    sharded_unpack_kernel<E_, G_><<<grid, 256, 0, st>>>(r, d, C);         \
     return finish_launch();
-#define UNPACK_E(E_)                                                                     \
-  case E_:                                                                               \
-    switch (1 << g) {                                                                    \
-      UNPACK_G(E_, 1) UNPACK_G(E_, 2) UNPACK_G(E_, 4) UNPACK_G(E_, 8)                    \
-      default:                                                                           \
-        sharded_unpack_generic_kernel<E_><<<(unsigned)elementwise_grid(C << g), 256, 0,  \
-                                            st>>>(r, d, C, g);                           \
-        return finish_launch();                                                          \
-    }
-  switch (E) { UNPACK_E(1) UNPACK_E(2) UNPACK_E(4) UNPACK_E(8) UNPACK_E(16) }
+#define UNPACK_E(E_)                                                            \
+  case E_:                                                                      \
+    switch (1 << g) { UNPACK_G(E_, 1) UNPACK_G(E_, 2) UNPACK_G(E_, 4) UNPACK_G(E_, 8) } \
+    break;
+    switch (E) { UNPACK_E(4) UNPACK_E(8) UNPACK_E(16) }
 #undef UNPACK_E
 #undef UNPACK_G
+  }
+  switch (E) {
+#define UNPACK_GEN(E_)                                                                    \
+  case E_:                                                                                \
+    sharded_unpack_generic_kernel<E_><<<(unsigned)elementwise_grid(C << g), 256, 0, st>>>( \
+        r, d, C, g);                                                                      \
+    return finish_launch();
+    UNPACK_GEN(1) UNPACK_GEN(2) UNPACK_GEN(4) UNPACK_GEN(8) UNPACK_GEN(16)
+#undef UNPACK_GEN
+  }
   return BITREV_EELEM;
 }
 

@@ -510,6 +510,7 @@ struct ScatterArgs {
   char* peer[kMaxPeers];  // receive buffer of each rank
   int g;                  // log2 G
   int rank;
+  int sb;                 // log2 of the sub-chunk length (= log2 C: one chunk)
 };
 
 template <int E, int Q>
@@ -541,7 +542,10 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS)
       const uint64_t u0 = ((uint64_t)(__brev((unsigned)z) >> (32 - Q)) << (a.b - Q)) | ry_base;
       const int d = (int)(u0 >> cbits);
       const uint64_t k0 = u0 & ((1ull << cbits) - 1);
-      st_vec(sa.peer[d] + (((uint64_t)sa.rank << cbits) + k0) * E + (uint64_t)col * 16, v);
+      // sub-chunk layout [c][rank][k']: k0 = c * 2^sb + k'
+      const uint64_t off = ((k0 >> sa.sb) << (sa.sb + sa.g)) | ((uint64_t)sa.rank << sa.sb) |
+                           (k0 & ((1ull << sa.sb) - 1));
+      st_vec(sa.peer[d] + off * E + (uint64_t)col * 16, v);
     }
     if (tn >= a.ntiles) break;
     __syncthreads();
@@ -1964,22 +1968,41 @@ __global__ void apply_pairs_kernel(char* a, const long long* pairs, int64_t npai
 
 // ---------------------------------------------------------------------------
 // sharded plan, step 3: dst[k*G + rev_g(r)] = recv[r*C + k].
-// One thread per k gathers the G values (coalesced across threads in k) and
-// writes its G*E contiguous destination bytes.
+// A thread owns K = 16/E consecutive k: one LDG.128 from each of the G source
+// chunks (coalesced across the warp), a register interleave, and G STG.128 of
+// its K*G*E contiguous destination bytes.  Needs C >= K and 16-byte aligned
+// buffers (the host falls back to the element-wise form otherwise).
 
 template <int E, int G>
-__global__ void sharded_unpack_kernel(const char* recv, char* dst, uint64_t C) {
-  using W = typename Word<E>::T;
+__global__ void __launch_bounds__(256) sharded_unpack_kernel(const char* recv, char* dst, uint64_t C) {
+  constexpr int K = 16 / E;   // k values per thread
+  constexpr int EW = E / 4;   // 32-bit words per element
   constexpr int LG = const_log2(G);
-  const W* rv = reinterpret_cast<const W*>(recv);
-  W* d = reinterpret_cast<W*>(dst);
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < C;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    W v[G];
+  const uint64_t nblk = C / K;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nblk;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t iw[G][4];  // word arrays with compile-time indices only: registers
 #pragma unroll
-    for (int r = 0; r < G; ++r) v[const_rev(r, LG)] = rv[(uint64_t)r * C + k];
+    for (int r = 0; r < G; ++r) {
+      const uint4 v = ld_stream(recv + ((uint64_t)r * C + t * K) * E);
+      iw[r][0] = v.x;
+      iw[r][1] = v.y;
+      iw[r][2] = v.z;
+      iw[r][3] = v.w;
+    }
+    uint32_t ow[4 * G];
 #pragma unroll
-    for (int s = 0; s < G; ++s) d[k * G + s] = v[s];
+    for (int kk = 0; kk < K; ++kk)
+#pragma unroll
+      for (int r = 0; r < G; ++r) {
+        const int rr = LG ? (int)(__brev((unsigned)r) >> (32 - LG)) : 0;  // folds after unrolling
+#pragma unroll
+        for (int j = 0; j < EW; ++j) ow[(kk * G + rr) * EW + j] = iw[r][kk * EW + j];
+      }
+    char* d = dst + t * (uint64_t)(K * G * E);
+#pragma unroll
+    for (int s = 0; s < G; ++s)
+      st_vec(d + s * 16, make_uint4(ow[4 * s], ow[4 * s + 1], ow[4 * s + 2], ow[4 * s + 3]));
   }
 }
 

@@ -8,7 +8,7 @@ and rev_{b-g}(j) = rev_g(l)*2^(b-2g) + rev_{b-2g}(m), so:
   1. local:  L = bitrev_{b-g}(shard)            -- the single-GPU tile kernel;
              L is already G contiguous chunks of C = 2^(b-2g) elements,
              chunk d destined for rank d = rev_g(l);
-  2. exchange: all-to-all with equal chunks      -- NCCL over NVLink/NVSwitch;
+  2. exchange: all_to_all_single, equal splits  -- NCCL over NVLink/NVSwitch;
              rank d receives recv[r] = L_r[d];
   3. local:  out[k*G + rev_g(r)] = recv[r][k]    -- bitrev_sharded_unpack.
 
@@ -53,6 +53,16 @@ def _local_bitrev(shard: torch.Tensor, b_local: int) -> torch.Tensor:
     return out
 
 
+def _pack(shard: torch.Tensor, b_local: int, g: int, kb: int) -> torch.Tensor:
+    """Step 1 into a new send buffer laid out [sub-chunk c][destination d][k']
+    (bitrev_sharded_pack); kb = 0 is the plain local reversal."""
+    send = torch.empty_like(shard)
+    with torch.cuda.device(shard.device):
+        _lib.call("bitrev_sharded_pack", shard.data_ptr(), send.data_ptr(), b_local, g, kb,
+                  _core.elem_bytes(shard), _core._stream_ptr(shard.device))
+    return send
+
+
 def _unpack(recv: torch.Tensor, b_local: int, g: int, out: torch.Tensor) -> None:
     """Step 3 into `out` (contiguous, recv-sized): out[k*G + rev_g(r)] = recv[r*C + k]."""
     with torch.cuda.device(recv.device):
@@ -60,25 +70,32 @@ def _unpack(recv: torch.Tensor, b_local: int, g: int, out: torch.Tensor) -> None
                   _core.elem_bytes(recv), _core._stream_ptr(recv.device))
 
 
-def _all_to_all(outs: list, ins: list, group):
-    """Async all-to-all of equal chunk lists; returns the work handle."""
-    return dist.all_to_all(outs, ins, group=group, async_op=True)
+def _all_to_all_single(out: torch.Tensor, inp: torch.Tensor, group):
+    """Equal-split all-to-all of one round (async); returns the work handle."""
+    return dist.all_to_all_single(out, inp, group=group, async_op=True)
 
 
 def sharded_bitrev(local: torch.Tensor, b: int, group=None, *, chunks: int = 1,
-                   local_permute: Callable | None = None,
+                   pack: Callable | None = None,
                    unpack: Callable | None = None,
-                   all_to_all: Callable | None = None) -> torch.Tensor:
+                   phases: dict | None = None) -> torch.Tensor:
     """Bit-reverse the global 2^b array whose rank-r shard is `local`.
 
     Returns this rank's shard of the permuted array (a new tensor).
-    chunks = K > 1 splits every destination chunk into K sub-chunks that are
-    exchanged as K asynchronous all-to-alls; sub-chunk c is interleaved (step
-    3) as soon as its exchange lands, while c+1.. are still on the wire.  The
-    output of step 3 for sub-chunk c is the contiguous slice
-    [c*C/K*G, (c+1)*C/K*G) of the local result, so no extra copies are made.
-    The step callables default to the CUDA kernels and NCCL; they are
-    injectable so the exchange logic can be exercised with gloo on CPU tensors.
+
+    Step 1 (pack) writes the local reversal as `chunks` = K rows of G*S
+    elements (S = C/K): row c holds sub-chunk c of every destination chunk, so
+    each row is the equal-split input of one `all_to_all_single` round.  The K
+    rounds are issued asynchronously; round c is interleaved (step 3) into the
+    contiguous output slice [c*S*G, (c+1)*S*G) as soon as it lands, while the
+    later rounds are still on the wire.  With K = 1 the pack is the plain
+    local reversal (bitrev_oop).
+
+    `pack(shard, b_local, g, kb)` and `unpack(recv, bits, g, out)` default to
+    the CUDA kernels; they are injectable so that the exchange itself (the
+    product's all_to_all_single rounds) runs under gloo on CPU tensors.
+    `phases`, if given, receives CUDA events "t0", "packed", "exchanged",
+    "done" recorded on the current stream (K = 1 only, for phase timing).
     """
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     g = check_plan(b, world)
@@ -88,26 +105,39 @@ def sharded_bitrev(local: torch.Tensor, b: int, group=None, *, chunks: int = 1,
     C = 1 << (b_local - g)
     if chunks < 1 or chunks & (chunks - 1) or chunks > C:
         raise ValueError(f"chunks must be a power of two in 1..{C}, got {chunks}")
-    local_permute = local_permute or _local_bitrev
+    kb = chunks.bit_length() - 1
+    pack = pack or _pack
     unpack = unpack or _unpack
-    all_to_all = all_to_all or _all_to_all
-    staged = local_permute(local.contiguous(), b_local)
+    timed = phases is not None and local.is_cuda
+
+    def mark(name):
+        if timed:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(torch.cuda.current_stream(local.device))
+            phases[name] = ev
+
+    mark("t0")
+    send = pack(local.contiguous(), b_local, g, kb)
+    mark("packed")
     if world == 1:
-        return staged
+        mark("exchanged")
+        mark("done")
+        return send
     G = world
     sub = C // chunks
-    kb = chunks.bit_length() - 1
-    recv = torch.empty_like(staged).view(chunks, G, sub)   # [sub-chunk][source rank][k]
-    out = torch.empty_like(staged)
-    works = []
-    for c in range(chunks):
-        ins = [staged[d * C + c * sub: d * C + (c + 1) * sub] for d in range(G)]
-        outs = [recv[c, r] for r in range(G)]
-        works.append(all_to_all(outs, ins, group))
+    recv = torch.empty_like(send)
+    sv, rv = send.view(chunks, G * sub), recv.view(chunks, G * sub)
+    works = [_all_to_all_single(rv[c], sv[c], group) for c in range(chunks)]
+    out = torch.empty_like(send)
     for c in range(chunks):
         if works[c] is not None:
             works[c].wait()
-        unpack(recv[c].reshape(-1), b_local - kb, g, out[c * sub * G:(c + 1) * sub * G])
+        if c == 0 and chunks == 1:
+            mark("exchanged")
+        unpack(rv[c], b_local - kb, g, out[c * sub * G:(c + 1) * sub * G])
+    if chunks > 1:
+        mark("exchanged")
+    mark("done")
     return out
 
 
@@ -129,7 +159,10 @@ def sharded_bitrev_p2p(local: torch.Tensor, b: int, peer_recv: list, rank: int,
     peers' buffers (bitrev_sharded_scatter: no send buffer, no NCCL pass);
     `barrier()` must order every rank's stores before any rank reads its
     buffer (a device-side or stream-synchronised cross-rank barrier); then the
-    interleave runs locally.  Returns this rank's shard of the permuted array.
+    interleave runs locally, and a second barrier keeps every rank's next
+    scatter out of the buffers until all unpacks have read them, so the same
+    buffers can be reused call after call.  Returns this rank's shard of the
+    permuted array.
     """
     world = len(peer_recv)
     g = check_plan(b, world)
@@ -137,9 +170,12 @@ def sharded_bitrev_p2p(local: torch.Tensor, b: int, peer_recv: list, rank: int,
     if local.dim() != 1 or local.shape[0] != (1 << b_local):
         raise ValueError(f"local shard length {local.shape[0]} does not match 2**{b_local}")
     _scatter(local.contiguous(), b_local, g, rank, peer_recv)
-    barrier()
+    barrier()  # every rank's stores into my buffer are done
     out = torch.empty_like(local)
     _unpack(peer_recv[rank], b_local, g, out)
+    # no rank may scatter its next call into my buffer before my unpack has
+    # read it (write-after-read across calls on the same symmetric buffers)
+    barrier()
     return out
 
 
@@ -182,9 +218,10 @@ def emulate_sharded_p2p(global_array: torch.Tensor, b: int, world_size: int) -> 
 def emulate_sharded(global_array: torch.Tensor, b: int, world_size: int,
                     chunks: int = 1) -> list[torch.Tensor]:
     """Run the three steps for `world_size` virtual ranks on ONE device, with
-    the exchange done by device copies (sub-chunked exactly like
-    sharded_bitrev).  Used to check the plan's kernels on a single GPU; the
-    real exchange is sharded_bitrev under torchrun."""
+    the exchange done by device copies (rounds exactly like sharded_bitrev:
+    the pack kernel's [c][d][k'] send layout, per-round unpack).  Used to
+    check the plan's kernels on a single GPU; the real exchange is
+    sharded_bitrev under torchrun."""
     g = check_plan(b, world_size)
     b_local = b - g
     S = 1 << b_local
@@ -192,13 +229,13 @@ def emulate_sharded(global_array: torch.Tensor, b: int, world_size: int,
     G = world_size
     sub = C // chunks
     kb = chunks.bit_length() - 1
-    staged = [_local_bitrev(global_array[r * S:(r + 1) * S].contiguous(), b_local)
-              for r in range(G)]
+    sends = [_pack(global_array[r * S:(r + 1) * S].contiguous(), b_local, g, kb).view(chunks, G, sub)
+             for r in range(G)]
     outs = []
     for d in range(G):
-        out = torch.empty_like(staged[0])
+        out = torch.empty_like(global_array[:S])
         for c in range(chunks):
-            recv = torch.cat([staged[r][d * C + c * sub:d * C + (c + 1) * sub] for r in range(G)])
+            recv = torch.cat([sends[r][c, d] for r in range(G)])
             _unpack(recv, b_local - kb, g, out[c * sub * G:(c + 1) * sub * G])
         outs.append(out)
     return outs

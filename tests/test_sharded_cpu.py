@@ -3,10 +3,11 @@
 1. A numpy simulation of the three steps (local reversal of b-g bits, equal
    chunk all-to-all, [G x C] -> [C x G] interleave with rev_g on rows) equals
    the oracle for many (b, G).
-2. The product's exchange logic, paper_1708_01873_b200.sharded.sharded_bitrev,
-   runs under torch.distributed with the gloo backend at world sizes 2 and 4;
-   the two local steps are injected as oracle-backed CPU callables (the CUDA
-   kernels behind them are covered by the GPU tests).
+2. The product's exchange, paper_1708_01873_b200.sharded.sharded_bitrev, runs
+   under torch.distributed with the gloo backend at world sizes 2 and 4: its
+   own all_to_all_single rounds move the data; only the two local CUDA steps
+   (pack, unpack) are injected as oracle-backed CPU callables (the kernels
+   behind them are covered by the GPU tests).
 """
 
 import os
@@ -65,6 +66,19 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def pack_np(shard, b_local, g, kb):
+    """Step 1 as the pack kernel lays it out: [sub-chunk c][destination d][k']."""
+    G, K = 1 << g, 1 << kb
+    S = 1 << (b_local - g - kb)
+    L = orc.oracle_permute(shard, b_local)           # L[d*C + c*S + k']
+    return np.ascontiguousarray(L.reshape(G, K, S).transpose(1, 0, 2)).reshape(-1)
+
+
+def test_pack_layout_is_plain_reversal_for_one_chunk():
+    x = np.arange(1 << 10, dtype=np.int64)
+    assert np.array_equal(pack_np(x, 10, 2, 0), orc.oracle_permute(x, 10))
+
+
 def _worker(rank, world, port, b, q, chunks=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -74,41 +88,22 @@ def _worker(rank, world, port, b, q, chunks=1):
         full = np.random.default_rng(b).integers(0, 1 << 60, 1 << b, dtype=np.int64)
         local = torch.from_numpy(full[rank << bl:(rank + 1) << bl].copy())
 
-        def local_permute(t, bits):
-            return torch.from_numpy(orc.oracle_permute(t.numpy(), bits))
+        # only the two local CUDA steps are replaced; the exchange is the
+        # product's own all_to_all_single rounds (gloo implements them)
+        def pack(t, bits, gg, kb):
+            return torch.from_numpy(pack_np(t.numpy(), bits, gg, kb))
 
         def unpack(recv, bits, gg, out):
             out.copy_(torch.from_numpy(unpack_np(recv.numpy(), bits, gg)))
 
-        class _Done:
-            def __init__(self, reqs):
-                self.reqs = reqs
-
-            def wait(self):
-                for r in self.reqs:
-                    r.wait()
-
-        def all_to_all(outs, ins, group):
-            # gloo has no list all_to_all (NCCL does): point-to-point exchange
-            reqs = []
-            me = dist.get_rank()
-            for peer in range(dist.get_world_size()):
-                if peer == me:
-                    outs[peer].copy_(ins[peer])
-                    continue
-                reqs.append(dist.isend(ins[peer].contiguous(), peer))
-                reqs.append(dist.irecv(outs[peer], peer))
-            return _Done(reqs)
-
-        out = sharded.sharded_bitrev(local, b, chunks=chunks, local_permute=local_permute,
-                                     unpack=unpack, all_to_all=all_to_all)
+        out = sharded.sharded_bitrev(local, b, chunks=chunks, pack=pack, unpack=unpack)
         expect = orc.oracle_permute(full, b)[rank << bl:(rank + 1) << bl]
         q.put((rank, bool(np.array_equal(out.numpy(), expect))))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,chunks", [(2, 1), (4, 1), (2, 4), (4, 2)])
+@pytest.mark.parametrize("world,chunks", [(2, 1), (4, 1), (2, 4), (4, 2), (4, 4)])
 def test_sharded_bitrev_gloo(world, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
