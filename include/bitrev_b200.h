@@ -169,6 +169,24 @@ int bitrev_sharded_scatter(const void* local, void* const* peer_recv, int b_loca
                            int elem_bytes, void* stream);
 
 /*
+ * apply_schedule with an explicit pair list whose pairs may share indices
+ * (replaces _apply_pairs, src/schedule.py:100-107): the pairs are swapped one
+ * after another in list order by a single device thread, so the result is
+ * the reference's for any list.  Indices must lie in [0, 2^b) (the Python
+ * layer checks).  Disjoint lists should use bitrev_apply_pairs.
+ */
+int bitrev_apply_pairs_ordered(void* a, const void* pairs, int64_t npairs, int elem_bytes,
+                               void* stream);
+
+/*
+ * The complete swap schedule of width b in the reference's emission order
+ * (generate_swap_schedule, src/schedule.py:77-91): swap_count(b) int64 pairs
+ * (i, rev_b(i)), i < rev_b(i), written to the device array pairs_out
+ * (2 * swap_count(b) int64).  Generated on the device, one thread per pair.
+ */
+int bitrev_swap_schedule(int b, void* pairs_out, void* stream);
+
+/*
  * Step 1 of the top-bit sharded plan for an all-to-all in 2^chunk_bits
  * rounds (no reference counterpart): the local reversal of
  * the 2^b_local-element shard written to `send` in the layout

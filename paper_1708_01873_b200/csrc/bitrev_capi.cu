@@ -839,6 +839,11 @@ int launch_scatter(const void* local, char* const* peer, int b_local, int g, int
   return BITREV_ETILE;
 }
 
+// swap_count (src/schedule.py:23-37) in closed form: (2^b - 2^ceil(b/2)) / 2
+uint64_t swap_count_dev_host(int b) {
+  return ((1ull << b) - (1ull << ((b + 1) >> 1))) >> 1;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1186,6 +1191,36 @@ int bitrev_apply_pairs(void* a, const void* pairs, int64_t npairs, int elem_byte
 #undef AP_CASE
   }
   return BITREV_EELEM;
+}
+
+int bitrev_apply_pairs_ordered(void* a, const void* pairs, int64_t npairs, int elem_bytes,
+                               void* stream) {
+  if (!valid_elem(elem_bytes)) return BITREV_EELEM;
+  if (npairs < 0) return BITREV_EBATCH;
+  if (npairs == 0) return BITREV_OK;
+  if (!a || !pairs) return BITREV_ENULL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long* pr = static_cast<const long long*>(pairs);
+  switch (elem_bytes) {
+#define APO_CASE(E_)                                                                    \
+  case E_:                                                                              \
+    apply_pairs_ordered_kernel<E_><<<1, 32, 0, st>>>(static_cast<char*>(a), pr, npairs); \
+    return finish_launch();
+    APO_CASE(1) APO_CASE(2) APO_CASE(4) APO_CASE(8) APO_CASE(16)
+#undef APO_CASE
+  }
+  return BITREV_EELEM;
+}
+
+int bitrev_swap_schedule(int b, void* pairs_out, void* stream) {
+  if (b < 1 || b > kMaxBits) return BITREV_EWIDTH;
+  if (!pairs_out) return BITREV_ENULL;
+  const uint64_t count = b <= 2 ? (uint64_t)(b - 1) : swap_count_dev_host(b);
+  if (count == 0) return BITREV_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  swap_schedule_kernel<<<(unsigned)elementwise_grid(count), 256, 0, st>>>(
+      static_cast<long long*>(pairs_out), b, count);
+  return finish_launch();
 }
 
 int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_t batch,

@@ -1966,6 +1966,58 @@ __global__ void apply_pairs_kernel(char* a, const long long* pairs, int64_t npai
   }
 }
 
+// In-order application of an arbitrary pair list by one thread: the exact
+// semantics of _apply_pairs (src/schedule.py:100-107) for lists whose pairs
+// share indices (the host checks; disjoint lists take apply_pairs_kernel).
+template <int E>
+__global__ void apply_pairs_ordered_kernel(char* a, const long long* pairs, int64_t npairs) {
+  using W = typename Word<E>::T;
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  W* p = reinterpret_cast<W*>(a);
+  for (int64_t k = 0; k < npairs; ++k) {
+    const long long i = pairs[2 * k], j = pairs[2 * k + 1];
+    const W t = p[i];
+    p[i] = p[j];
+    p[j] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// swap schedule of width b in the reference's emission order
+// (generate_swap_schedule / _fill_pairs, src/schedule.py:53-91).  The
+// generator is an in-order walk of a binary tree: the node at depth d with
+// outer-bit path `base` emits 2^(b-2d-2) pairs (middle value x ascending),
+// after its (0,0) subtree and before its (1,1) subtree; a subtree rooted at
+// depth d holds swap_count(b - 2d) pairs.  One thread per output slot k
+// descends the tree to find its node and x -- O(b) integer work, no list.
+
+__device__ __forceinline__ uint64_t swap_count_dev(int r) {
+  return r <= 0 ? 0ull : (((1ull << r) - (1ull << ((r + 1) >> 1))) >> 1);
+}
+
+__global__ void swap_schedule_kernel(long long* out, int b, uint64_t count) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t base = 0, start = 0;
+    for (int depth = 0;; ++depth) {
+      const int rem = b - 2 * depth;
+      const uint64_t left = swap_count_dev(rem - 2);
+      const uint64_t lo_bit = 1ull << depth, hi_bit = 1ull << (b - 1 - depth);
+      if (k < start + left) continue;  // into the (0,0) subtree: same start, same base
+      const uint64_t blk = 1ull << (rem - 2);
+      if (k < start + left + blk) {
+        const uint64_t x = k - start - left;
+        const int mid = rem - 2;
+        out[2 * k] = (long long)(base | (x << (depth + 1)) | lo_bit);
+        out[2 * k + 1] = (long long)(base | (dev_rev(x, mid) << (depth + 1)) | hi_bit);
+        break;
+      }
+      start += left + blk;  // into the (1,1) subtree
+      base |= lo_bit | hi_bit;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // sharded plan, step 3: dst[k*G + rev_g(r)] = recv[r*C + k].
 // A thread owns K = 16/E consecutive k: one LDG.128 from each of the G source

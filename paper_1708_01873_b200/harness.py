@@ -4,9 +4,9 @@
 make_method (src/bench.py:135-185) is the uniform (array, b) adapter the
 reference's tests and acceptance suite drive; METHOD_IDS / ELEMENT_KINDS /
 fill keep the reference's ids, dtypes and seeded distributions so GPU and CPU
-runs see identical inputs.  run_benchmark times methods on the device with CUDA
-events and emits records in the reference CSV schema (src/bench.py:436-473), so
-the reference tooling (read_csv, plotkit) reads GPU series unchanged.
+runs see identical inputs.  Records use the reference CSV schema
+(src/bench.py:436-473), so the reference tooling (read_csv, plotkit) reads GPU
+series unchanged; the benchmark driver itself is benchmark.py.
 """
 
 from __future__ import annotations
@@ -170,34 +170,4 @@ def read_csv(path) -> list[BenchmarkRecord]:
             if rec.n != int(n):
                 raise ValueError(f"{path}:{lineno}: n={n} does not match 2**{b}")
             records.append(rec)
-    return records
-
-
-def run_benchmark(methods=("cobra", "cobra_inplace"), b_min: int = 8, b_max: int = 20,
-                  replicates: int = 10, warmup: int = 3, element_kind: str = "pair",
-                  seed: int = 0, flush_l2: bool = True) -> list[BenchmarkRecord]:
-    """Time methods on the current CUDA device with CUDA events; one record per
-    replicate, reference schema.  The L2 is flushed between replicates unless
-    flush_l2 is False (then small sizes are L2-hot)."""
-    dev = torch.device("cuda", torch.cuda.current_device())
-    dtype = ELEMENT_KINDS[element_kind]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush_l2 else None
-    records = []
-    for b in range(b_min, b_max + 1):
-        for method in methods:
-            fn = make_method(method)
-            host = fill_numpy(1 << b, element_kind, seed, method, b, -1)
-            a = torch.from_numpy(host).to(dev)
-            for _ in range(warmup):
-                fn(a, b)
-            for rep in range(replicates):
-                if flush is not None:
-                    flush.zero_()
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s.record()
-                fn(a, b)
-                e.record()
-                e.synchronize()
-                records.append(make_record(method, b, rep, s.elapsed_time(e) / 1e3))
-    del dtype
     return records

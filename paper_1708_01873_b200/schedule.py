@@ -1,17 +1,19 @@
-"""Swap-schedule entry points of src/schedule.py that sit on the hot path.
+"""Swap schedules (src/schedule.py): the explicit pair lists that realize the
+permutation, and their replay.
 
-A complete schedule for width b ({(i, rev i): i < rev i}) applied in any order
-IS the permutation, so apply_schedule with a complete schedule takes the tile
-kernel; an explicit caller-supplied pair list is replayed by the pair kernel
-(bitrev_apply_pairs).  Schedule *generation* (the branch-and-bound _fill_pairs,
-the BRSCHD01 file format) is a CPU base-case device of the reference and is out
-of scope; swap_count is kept because it is the counting law the
-tests pin.
+A schedule of width b lists every (i, rev i) with i < rev i; swapping the
+pairs in any order IS the permutation.  generate_swap_schedule /
+cached_schedule return the reference's pair array in its emission order
+(_fill_pairs, src/schedule.py:53-91), generated on the device by
+bitrev_swap_schedule (one thread per pair, no host loop), as a read-only
+(count, 2) int64 CUDA tensor.  apply_schedule replays a complete schedule
+with the tile kernels (its pairs need not even be materialised), an explicit
+disjoint list with the pair kernel, and a list whose pairs share indices in
+list order, exactly like _apply_pairs (src/schedule.py:100-107).
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
 from functools import lru_cache
 
 import numpy as np
@@ -32,39 +34,74 @@ def swap_count(b: int) -> int:
     return (1 << (b - 2)) + 2 * swap_count(b - 2)
 
 
-@dataclass(frozen=True)
-class SwapSchedule:
-    """Width plus an optional (count, 2) int64 pair array.
+def _device_pairs(b: int, device=None) -> torch.Tensor:
+    dev = torch.device(device) if device is not None else _core.require_cuda()
+    out = torch.empty((swap_count(b), 2), dtype=torch.int64, device=dev)
+    if out.numel():
+        with torch.cuda.device(dev):
+            _lib.call("bitrev_swap_schedule", b, out.data_ptr(), _core._stream_ptr(dev))
+    return out
 
-    pairs=None denotes the complete schedule for width b (what cached_schedule
-    returns); an explicit array is replayed pair by pair.
+
+class SwapSchedule:
+    """Width plus the (count, 2) int64 array of (lo, hi) index pairs
+    (src/schedule.py:40-51).
+
+    `complete=True` marks the full schedule of width b (what
+    generate_swap_schedule / cached_schedule return): its pairs are built on
+    the device the first time `.pairs` is read, and apply_schedule runs it as
+    the tile-kernel permutation.  A caller-supplied array (numpy or torch) is
+    kept as given and replayed pair by pair.
     """
 
-    b: int
-    pairs: np.ndarray | torch.Tensor | None = None
+    __slots__ = ("b", "_pairs", "complete")
 
-    def __post_init__(self):
-        if self.pairs is not None and (self.pairs.ndim != 2 or self.pairs.shape[1] != 2):
+    def __init__(self, b: int, pairs=None, complete: bool | None = None):
+        if pairs is None and complete is False:
+            raise ValueError("an incomplete schedule needs its pairs")
+        if pairs is not None and (pairs.ndim != 2 or pairs.shape[1] != 2):
             raise ValueError("pairs must have shape (count, 2)")
+        self.b = b
+        self._pairs = pairs
+        self.complete = pairs is None if complete is None else complete
+
+    @property
+    def pairs(self):
+        if self._pairs is None:
+            self._pairs = _device_pairs(self.b)
+        return self._pairs
 
     def __len__(self) -> int:
-        return swap_count(self.b) if self.pairs is None else len(self.pairs)
+        return swap_count(self.b) if self._pairs is None else len(self._pairs)
+
+    def __repr__(self) -> str:
+        return f"SwapSchedule(b={self.b}, pairs={len(self)}, complete={self.complete})"
+
+
+def generate_swap_schedule(b: int, max_bits: int = SCHEDULE_MAX_BITS) -> SwapSchedule:
+    """All (i, rev i) pairs with i < rev i for width b, in the reference's
+    emission order: depth first, the 0-prefix branch before the 1-prefix
+    branch, middle values ascending (src/schedule.py:77-91)."""
+    if not 1 <= b <= max_bits:
+        raise ValueError(f"schedule width must be in 1..{max_bits}, got {b}")
+    return SwapSchedule(b, _device_pairs(b), complete=True)
 
 
 @lru_cache(maxsize=None)
 def cached_schedule(b: int) -> SwapSchedule:
-    """The complete schedule for width b (src/schedule.py:94-97)."""
+    """Shared schedule per width (src/schedule.py:94-97); pairs on first use."""
     if not 1 <= b <= SCHEDULE_MAX_BITS:
         raise ValueError(f"schedule width must be in 1..{SCHEDULE_MAX_BITS}, got {b}")
-    return SwapSchedule(b)
+    return SwapSchedule(b, None, complete=True)
 
 
 def apply_schedule(array, schedule: SwapSchedule) -> None:
     """Swap every scheduled pair in place (src/schedule.py:124-130)."""
     a = as_tensor(array)
-    if a.shape[0] != (1 << schedule.b):
+    n = 1 << schedule.b
+    if a.shape[0] != n:
         raise ValueError(f"array length {a.shape[0]} does not match 2**{schedule.b}")
-    if schedule.pairs is None:
+    if schedule.complete:
         _core.permute_inplace(a, schedule.b)
         return
     if not a.is_cuda:
@@ -72,9 +109,19 @@ def apply_schedule(array, schedule: SwapSchedule) -> None:
         apply_schedule(work, schedule)
         a.copy_(work)
         return
-    pairs = torch.as_tensor(schedule.pairs, dtype=torch.int64).to(a.device).contiguous()
     if not a.is_contiguous():
         raise ValueError("apply_schedule with explicit pairs needs a contiguous array")
+    p = schedule.pairs
+    pairs = (torch.from_numpy(np.ascontiguousarray(p, dtype=np.int64)) if isinstance(p, np.ndarray)
+             else p.to(torch.int64)).to(a.device).contiguous()
+    if pairs.numel() == 0:
+        return
+    lo, hi = torch.aminmax(pairs)
+    if int(lo) < 0 or int(hi) >= n:
+        raise ValueError(f"schedule pairs must index [0, 2**{schedule.b})")
+    flat = pairs.reshape(-1)
+    disjoint = torch.unique(flat).numel() == flat.numel()
+    name = "bitrev_apply_pairs" if disjoint else "bitrev_apply_pairs_ordered"
     with torch.cuda.device(a.device):
-        _lib.call("bitrev_apply_pairs", a.data_ptr(), pairs.data_ptr(), pairs.shape[0],
-                  _core.elem_bytes(a), _core._stream_ptr(a.device))
+        _lib.call(name, a.data_ptr(), pairs.data_ptr(), pairs.shape[0], _core.elem_bytes(a),
+                  _core._stream_ptr(a.device))

@@ -187,3 +187,60 @@ def test_csv_round_trip(tmp_path):
     br.write_csv(recs, p)
     assert br.read_csv(p) == recs
     assert p.read_text().splitlines()[0] == "method,b,n,replicate,elapsed_s,per_element_s"
+
+
+# --- benchmark API (src/bench.py:69-110, 380-433) ----------------------------
+
+
+def test_bench_config_defaults_match_reference_fields():
+    cfg = br.BenchConfig()
+    assert cfg.methods == br.METHOD_IDS and (cfg.b_min, cfg.b_max) == (8, 20)
+    assert (cfg.replicates, cfg.warmup, cfg.element_kind) == (100, 3, "pair")
+    assert cfg.memory_cap_bytes == 1 << 30 and cfg.unrolled_max_bits == 16
+    br.validate_config(cfg)
+
+
+@pytest.mark.parametrize("kw,frag", [
+    ({"methods": ()}, "no methods"),
+    ({"methods": ("cobra", "nope")}, "unknown methods"),
+    ({"b_min": 9, "b_max": 8}, "b_min"),
+    ({"replicates": 0}, "replicates"),
+    ({"warmup": -1}, "warmup"),
+    ({"element_kind": "c64"}, "element kind"),
+    ({"cobra_q": -1}, "cobra_q"),
+    ({"memory_cap_bytes": 0}, "memory_cap_bytes"),
+    ({"base_bits": 0}, ""),
+])
+def test_bench_config_validation(kw, frag):
+    with pytest.raises(ValueError, match=frag):
+        br.validate_config(br.BenchConfig(**kw))
+
+
+def test_tune_cobra_argument_checks():
+    with pytest.raises(ValueError, match="must not be empty"):
+        br.tune_cobra(10, [])
+    with pytest.raises(ValueError, match="violate"):
+        br.tune_cobra(10, [3, 6])
+    with pytest.raises(ValueError, match="variant"):
+        br.tune_cobra(10, [3], variant="stockham")
+    with pytest.raises(ValueError, match="replicates"):
+        br.tune_cobra(10, [3], replicates=0)
+
+
+def test_gbs_sidecar(tmp_path):
+    recs = [br.make_record("cobra", 20, r, 1e-5) for r in range(2)]
+    p = tmp_path / "gbs.csv"
+    br.write_gbs_sidecar(recs, p, "pair")
+    rows = p.read_text().splitlines()
+    assert rows[0] == "method,b,n,replicate,elem_bytes,bytes_moved,gb_per_s,gelem_per_s"
+    f = rows[1].split(",")
+    assert f[4] == "16" and int(f[5]) == 2 * (1 << 20) * 16
+    assert abs(float(f[6]) - 2 * (1 << 20) * 16 / 1e-5 / 1e9) < 1e-6
+
+
+def test_complete_schedule_is_lazy():
+    s = br.cached_schedule(20)
+    assert s.complete and len(s) == br.swap_count(20)
+    assert s._pairs is None  # nothing materialised until .pairs is read
+    e = br.SwapSchedule(3, np.array([[1, 4], [3, 6]]))
+    assert not e.complete and len(e) == 2
