@@ -1,0 +1,181 @@
+// DRAM efficiency vs contiguous run length on B200 (measurement probe, not
+// product code).  Question it answers: how much of the measured copy peak can
+// a permutation of R-byte runs reach, out of place and in place (pairwise
+// swaps), as a function of R -- the in-place tile-pair kernel moves 512-byte
+// runs (E=8, Q=6) on both sides.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o runs runs.cu && ./runs
+//
+// Kernels (all persistent, 16-byte vectors, U blocks in flight per lane group):
+//   copy   : linear copy (the same-size ceiling)
+//   oop<R> : dst block rev(k) <- src block k          (bit-reversed block order)
+//   mul<R> : dst block (k*A mod nb) <- src block k      (odd multiplier A)
+//   swap<R>: in place, blocks k <-> rev(k) for k < rev(k)
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint4 ldg(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ldp(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint64_t rev(uint64_t v, int w) { return w ? __brevll(v) >> (64 - w) : 0; }
+
+__global__ void __launch_bounds__(256) copy_lin(const uint4* s, uint4* d, uint64_t nv) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < nv; i += 4 * stride) {
+    uint4 a = ldg(s + i), b = ldg(s + i + stride), c = ldg(s + i + 2 * stride),
+          e = ldg(s + i + 3 * stride);
+    stg(d + i, a); stg(d + i + stride, b); stg(d + i + 2 * stride, c); stg(d + i + 3 * stride, e);
+  }
+  for (; i < nv; i += stride) stg(d + i, ldg(s + i));
+}
+
+// MODE 0: dst rev(k) <- src k; MODE 1: dst (k*A mod nb) <- src k
+template <int R, int U, int MODE>
+__global__ void __launch_bounds__(256) blk_oop(const char* s, char* d, int lb) {
+  constexpr int G = R / 16 < 32 ? R / 16 : 32;   // lanes per block
+  constexpr int VPL = R / 16 / G;                 // vectors per lane per block
+  constexpr int BPW = 32 / G;                     // blocks per warp per step
+  const uint64_t nb = 1ull << lb;
+  const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t k0 = warp * BPW * U; k0 < nb; k0 += nwarps * BPW * U) {
+    uint4 v[U][VPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = k0 + u * BPW + sub;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) v[u][j] = ldg(s + k * R + (j * G + gl) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = k0 + u * BPW + sub;
+      const uint64_t t = MODE == 0 ? rev(k, lb) : ((k * 0x9E3779B1ull) & (nb - 1));
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) stg(d + t * R + (j * G + gl) * 16, v[u][j]);
+    }
+  }
+}
+
+template <int R, int U>
+__global__ void __launch_bounds__(256) blk_swap(char* a, int lb) {
+  constexpr int G = R / 16 < 32 ? R / 16 : 32;
+  constexpr int VPL = R / 16 / G;
+  constexpr int BPW = 32 / G;
+  const uint64_t nb = 1ull << lb;
+  const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  // items: every k visited, k > rev(k) lanes idle (half the items), so the
+  // work per warp is balanced on average
+  for (uint64_t k0 = warp * BPW * U; k0 < nb; k0 += nwarps * BPW * U) {
+    uint4 v[U][VPL], w[U][VPL];
+    bool act[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = k0 + u * BPW + sub, r = rev(k, lb);
+      act[u] = k <= r;
+      if (act[u]) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          v[u][j] = ldp(a + k * R + (j * G + gl) * 16);
+          w[u][j] = ldp(a + r * R + (j * G + gl) * 16);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = k0 + u * BPW + sub, r = rev(k, lb);
+      if (act[u]) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          stg(a + r * R + (j * G + gl) * 16, v[u][j]);
+          stg(a + k * R + (j * G + gl) * 16, w[u][j]);
+        }
+      }
+    }
+  }
+}
+
+template <typename F>
+double time_ms(F f, int reps) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  f();
+  f();
+  cudaDeviceSynchronize();
+  std::vector<float> ts;
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(e0);
+    f();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ts.push_back(ms);
+  }
+  std::sort(ts.begin(), ts.end());
+  return ts[ts.size() / 2];
+}
+
+template <int R, int U>
+void run_r(char* s, char* d, uint64_t bytes, int sms, int cps) {
+  int lb = 0;
+  while ((uint64_t(R) << (lb + 1)) <= bytes) ++lb;
+  const uint64_t used = uint64_t(R) << lb;
+  const int grid = sms * cps;
+  double t0 = time_ms([&] { blk_oop<R, U, 0><<<grid, 256>>>(s, d, lb); }, 15);
+  double t1 = time_ms([&] { blk_oop<R, U, 1><<<grid, 256>>>(s, d, lb); }, 15);
+  double t2 = time_ms([&] { blk_swap<R, U><<<grid, 256>>>(d, lb); }, 15);
+  printf("{\"bytes\": %llu, \"R\": %d, \"U\": %d, \"oop_rev_gbs\": %.1f, \"oop_mul_gbs\": %.1f, "
+         "\"swap_rev_gbs\": %.1f}\n",
+         (unsigned long long)used, R, U, 2.0 * used / t0 / 1e6, 2.0 * used / t1 / 1e6,
+         2.0 * used / t2 / 1e6);
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (uint64_t bytes : {512ull << 20, 4096ull << 20}) {
+    char *s, *d;
+    cudaMalloc(&s, bytes);
+    cudaMalloc(&d, bytes);
+    cudaMemset(s, 1, bytes);
+    cudaMemset(d, 2, bytes);
+    const uint64_t nv = bytes / 16;
+    for (int cps : {4, 8}) {
+      double t = time_ms([&] { copy_lin<<<sms * cps, 256>>>((const uint4*)s, (uint4*)d, nv); }, 15);
+      printf("{\"bytes\": %llu, \"copy_ctas_per_sm\": %d, \"copy_gbs\": %.1f}\n",
+             (unsigned long long)bytes, cps, 2.0 * bytes / t / 1e6);
+    }
+    run_r<256, 4>(s, d, bytes, sms, 8);
+    run_r<512, 4>(s, d, bytes, sms, 8);
+    run_r<1024, 2>(s, d, bytes, sms, 8);
+    run_r<2048, 2>(s, d, bytes, sms, 8);
+    run_r<4096, 1>(s, d, bytes, sms, 8);
+    run_r<8192, 1>(s, d, bytes, sms, 4);
+    cudaFree(s);
+    cudaFree(d);
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("{\"status\": \"%s\"}\n", cudaGetErrorString(e));
+  return 0;
+}
