@@ -839,6 +839,29 @@ int launch_scatter(const void* local, char* const* peer, int b_local, int g, int
   return BITREV_ETILE;
 }
 
+cudaStream_t st_of(void* stream) { return static_cast<cudaStream_t>(stream); }
+
+template <int E, int QX, int QZ>
+int launch_pack_rect(const void* src, void* dst, int b, int g, int sb, cudaStream_t st) {
+  using T = Rect<E, QX, QZ>;
+  if (b < QX + QZ || sb < QX) return BITREV_ETILE;
+  auto kern = bitrev_pack_rect_kernel<E, QX, QZ>;
+  const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
+  PackArgs pa;
+  memset(&pa, 0, sizeof pa);
+  TileArgs& a = pa.t;
+  a.src = static_cast<const char*>(src);
+  a.dst = static_cast<char*>(dst);
+  a.b = b;
+  a.m = b - QX - QZ;
+  a.ntiles = 1ull << a.m;
+  a.batch = 1;
+  pa.g = g;
+  pa.sb = sb;
+  kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(pa);
+  return finish_launch();
+}
+
 // swap_count (src/schedule.py:23-37) in closed form: (2^b - 2^ceil(b/2)) / 2
 uint64_t swap_count_dev_host(int b) {
   return ((1ull << b) - (1ull << ((b + 1) >> 1))) >> 1;
@@ -1370,6 +1393,14 @@ int bitrev_sharded_pack(const void* local, void* send, int b_local, int g, int c
   if (chunk_bits == 0)  // one chunk: the send layout is the plain reversal
     return bitrev_oop(local, send, b_local, E, 1, 0, 0, stream);
   const int sb = b_local - g - chunk_bits;
+  if (aligned16(local) && aligned16(send)) {
+    // rectangular tiles with re-addressed rows (1 KB destination rows)
+    int rc = BITREV_ETILE;
+    if (E == 4) rc = launch_pack_rect<4, 8, 6>(local, send, b_local, g, sb, st_of(stream));
+    if (E == 8) rc = launch_pack_rect<8, 7, 5>(local, send, b_local, g, sb, st_of(stream));
+    if (E == 16) rc = launch_pack_rect<16, 6, 6>(local, send, b_local, g, sb, st_of(stream));
+    if (rc != BITREV_ETILE) return rc;
+  }
   char* peer[kMaxPeers] = {};
   for (int d = 0; d < (1 << g); ++d) peer[d] = static_cast<char*>(send) + ((uint64_t)E << sb) * d;
   return launch_scatter(local, peer, b_local, g, 0, sb, E, static_cast<cudaStream_t>(stream));

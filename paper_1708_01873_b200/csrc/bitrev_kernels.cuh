@@ -46,16 +46,13 @@
 
 // Build-time tuning knobs (defaults are the measured best).  Alternatives are
 // built side by side with `python -m paper_1708_01873_b200.build --out F -DKNOB=V`
-// and loaded through BITREV_B200_LIB for A/B runs (tools/*_ab.py).  The two
-// EXPERIMENT knobs produce WRONG output on purpose (timing-only builds).
+// and loaded through BITREV_B200_LIB for A/B runs (tools/*_ab.py).  Every knob
+// value produces the same (correct) output.
 #ifndef BITREV_IP_NC
 #define BITREV_IP_NC 0  // in-place loads through the non-coherent path
 #endif
 #ifndef BITREV_MINB_OOP
 #define BITREV_MINB_OOP 1  // __launch_bounds__ min CTAs/SM, out-of-place tile kernel
-#endif
-#ifndef BITREV_EXPERIMENT_CONTIG
-#define BITREV_EXPERIMENT_CONTIG 0  // timing experiment only: partner = y ^ 1 (WRONG output)
 #endif
 #ifndef BITREV_TILE_THREADS
 #define BITREV_TILE_THREADS 256  // threads per CTA of the register tile kernels
@@ -71,9 +68,6 @@
 #endif
 #ifndef BITREV_RING_BUDGET_KB
 #define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
-#endif
-#ifndef BITREV_EXPERIMENT_ROWPAD
-#define BITREV_EXPERIMENT_ROWPAD 0  // timing experiment only: bytes added to the row stride
 #endif
 #ifndef BITREV_MINB_IP
 #define BITREV_MINB_IP 1  // __launch_bounds__ min CTAs/SM, in-place tile kernel
@@ -376,7 +370,7 @@ __global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, BITREV_MINB_OOP)
     bitrev_oop_tile_kernel(TileArgs a) {
   using T = Tile<E, Q, NT>;
   extern __shared__ __align__(16) uint4 smem[];
-  const uint64_t row_stride = ((uint64_t)E << (a.b - Q)) + BITREV_EXPERIMENT_ROWPAD;
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
   const uint64_t mmask = (1ull << a.m) - 1;
   uint4 r[T::IPT][T::V];
 
@@ -492,6 +486,80 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
 }
 
 // ---------------------------------------------------------------------------
+// sharded plan, step 1 for an all-to-all in K = 2^kb rounds: the rectangular
+// tile kernel above with its destination rows re-addressed.  Local output
+// index u = d * C + c * S + k' (d = destination rank, c = round, S = 2^sb)
+// is stored at u' = c * G * S + d * S + k', so that round c's send data is
+// the contiguous slice [c * G * S, (c + 1) * G * S) with equal per-rank
+// splits.  A destination row (2^QX contiguous u) never straddles a
+// sub-chunk (S >= 2^QX), so the remap costs a few integer ops per row.
+
+struct PackArgs {
+  TileArgs t;
+  int g;   // log2 G
+  int sb;  // log2 S
+};
+
+template <int E, int QX, int QZ>
+__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
+    bitrev_pack_rect_kernel(PackArgs pa) {
+  using T = Rect<E, QX, QZ>;
+  extern __shared__ __align__(16) uint4 smem[];
+  const TileArgs& a = pa.t;
+  const uint64_t src_row = (uint64_t)E << (a.b - QX);
+  const int db = a.b - pa.g;  // bits of u below the rank field
+  const uint64_t smask = (1ull << pa.sb) - 1, cmask = (1ull << db) - 1;
+  uint4 r[T::IPT][T::V];
+
+  auto load = [&](uint64_t y) {
+    const char* base = a.src + (y << QZ) * E;
+#pragma unroll
+    for (int it = 0; it < T::IPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int c = id % T::CZ, g = id / T::CZ;
+#pragma unroll
+      for (int k = 0; k < T::V; ++k)
+        r[it][k] = ld_stream(base + (uint64_t)(g + k * T::GX) * src_row + (uint64_t)c * 16);
+    }
+  };
+  auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
+
+  uint64_t t = blockIdx.x;
+  if (t >= a.ntiles) return;
+  load(t);
+  for (;;) {
+#pragma unroll
+    for (int it = 0; it < T::IPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int c = id % T::CZ, g = id / T::CZ;
+      const int col = (int)(__brev((unsigned)g) >> (32 - (QX - T::LV)));
+      smem[sidx(c * T::V, col)] = xpose<E, 0>(r[it]);
+      if constexpr (T::V > 1) smem[sidx(c * T::V + 1, col)] = xpose<E, 1>(r[it]);
+      if constexpr (T::V > 2) {
+        smem[sidx(c * T::V + 2, col)] = xpose<E, 2>(r[it]);
+        smem[sidx(c * T::V + 3, col)] = xpose<E, 3>(r[it]);
+      }
+    }
+    __syncthreads();
+    const uint64_t tn = t + gridDim.x;
+    if (tn < a.ntiles) load(tn);
+    const uint64_t ry = dev_rev(t, a.m) << QX;
+#pragma unroll
+    for (int it = 0; it < T::WPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int col = id % T::GX, z = id / T::GX;
+      const uint64_t u = ((uint64_t)(__brev((unsigned)z) >> (32 - QZ)) << (a.b - QZ)) | ry;
+      const uint64_t rest = u & cmask;
+      const uint64_t up = ((rest >> pa.sb) << (pa.sb + pa.g)) | ((u >> db) << pa.sb) | (rest & smask);
+      st_vec<true>(a.dst + up * E + (uint64_t)col * 16, smem[sidx(z, col)]);
+    }
+    if (tn >= a.ntiles) break;
+    __syncthreads();
+    t = tn;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // sharded plan, steps 1+2 fused: local bit reversal scattered to peers
 //
 // Rank `rank` of G = 2^g reverses its (b-g)-bit shard; the local output index
@@ -571,13 +639,11 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
   extern __shared__ __align__(16) uint4 smem[];
   uint4* U0 = smem;
   uint4* U1 = smem + T::WCH;
-  const uint64_t row_stride = ((uint64_t)E << (a.b - Q)) + BITREV_EXPERIMENT_ROWPAD;
+  const uint64_t row_stride = (uint64_t)E << (a.b - Q);
   const uint64_t mmask = (1ull << a.m) - 1;
   uint4 r0[T::IPT][T::V], r1[T::IPT][T::V];
 
-  auto partner = [&](uint64_t y) {
-    return BITREV_EXPERIMENT_CONTIG ? (y ^ 1ull) : dev_rev(y, a.m);
-  };
+  auto partner = [&](uint64_t y) { return dev_rev(y, a.m); };
   // Work cursor: COMPACT walks the pair enumeration (one item per pair);
   // otherwise every y is visited in `order` and items with rev(y) < y skipped.
   PairCursor pc;
@@ -2020,19 +2086,33 @@ __global__ void swap_schedule_kernel(long long* out, int b, uint64_t count) {
 
 // ---------------------------------------------------------------------------
 // sharded plan, step 3: dst[k*G + rev_g(r)] = recv[r*C + k].
-// A thread owns K = 16/E consecutive k: one LDG.128 from each of the G source
-// chunks (coalesced across the warp), a register interleave, and G STG.128 of
-// its K*G*E contiguous destination bytes.  Needs C >= K and 16-byte aligned
-// buffers (the host falls back to the element-wise form otherwise).
+// A lane owns K = 16/E consecutive k: one LDG.128 from each of the G source
+// chunks (coalesced across the warp: 512 B per chunk per instruction) and a
+// register interleave into its G output chunks (K*G*E contiguous bytes).  The
+// warp's 32*G output chunks are contiguous, so they go out through a per-warp
+// shared-memory bounce (XOR-swizzled, conflict-free both ways) as G fully
+// coalesced 512-byte STG.128 rows instead of G strided ones (the strided
+// stores ran at 0.43 of the HBM peak for G = 8).  Needs C >= K and 16-byte
+// aligned buffers (the host falls back to the element-wise form otherwise).
+
+template <int G>
+__device__ __forceinline__ int unpack_swz(int c) { return c ^ ((c >> 3) & 7); }
 
 template <int E, int G>
 __global__ void __launch_bounds__(256) sharded_unpack_kernel(const char* recv, char* dst, uint64_t C) {
-  constexpr int K = 16 / E;   // k values per thread
+  constexpr int K = 16 / E;   // k values per lane
   constexpr int EW = E / 4;   // 32-bit words per element
   constexpr int LG = const_log2(G);
+  constexpr int WARPS = 8;
+  __shared__ uint4 bounce[WARPS][32 * G];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint4* my = bounce[wid];
   const uint64_t nblk = C / K;
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nblk;
-       t += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
+  for (uint64_t wb = ((uint64_t)blockIdx.x * WARPS + wid) * 32; wb < nblk; wb += nwarps * 32) {
+    const uint64_t t = wb + lane;
+    const bool full = wb + 32 <= nblk;  // warp-uniform
+    if (!full && t >= nblk) continue;
     uint32_t iw[G][4];  // word arrays with compile-time indices only: registers
 #pragma unroll
     for (int r = 0; r < G; ++r) {
@@ -2051,10 +2131,21 @@ __global__ void __launch_bounds__(256) sharded_unpack_kernel(const char* recv, c
 #pragma unroll
         for (int j = 0; j < EW; ++j) ow[(kk * G + rr) * EW + j] = iw[r][kk * EW + j];
       }
-    char* d = dst + t * (uint64_t)(K * G * E);
+    if (full) {
 #pragma unroll
-    for (int s = 0; s < G; ++s)
-      st_vec(d + s * 16, make_uint4(ow[4 * s], ow[4 * s + 1], ow[4 * s + 2], ow[4 * s + 3]));
+      for (int s = 0; s < G; ++s)
+        my[unpack_swz<G>(lane * G + s)] = make_uint4(ow[4 * s], ow[4 * s + 1], ow[4 * s + 2], ow[4 * s + 3]);
+      __syncwarp();
+      char* d = dst + wb * (uint64_t)(K * G * E);
+#pragma unroll
+      for (int j = 0; j < G; ++j) st_vec(d + (j * 32 + lane) * 16, my[unpack_swz<G>(j * 32 + lane)]);
+      __syncwarp();
+    } else {  // ragged last warp: direct (strided) stores
+      char* d = dst + t * (uint64_t)(K * G * E);
+#pragma unroll
+      for (int s = 0; s < G; ++s)
+        st_vec(d + s * 16, make_uint4(ow[4 * s], ow[4 * s + 1], ow[4 * s + 2], ow[4 * s + 3]));
+    }
   }
 }
 

@@ -43,8 +43,12 @@ def bitrev_dit_prepass(x, b: int, stages: int, inverse: bool = False, out=None) 
     if _core.shares_memory(t, dst):
         raise ValueError("x and out must not overlap")
     if t.is_cuda:
-        src_d, dst_d = t.contiguous(), (dst if dst.is_contiguous() else torch.empty_like(t))
         dev = t.device
+        src_d = t.contiguous()
+        # the kernel writes dst_d on x's device: anything else (a host or numpy
+        # out, another GPU, a strided view) gets a device temporary copied back
+        same = isinstance(dst, torch.Tensor) and dst.device == dev and dst.is_contiguous()
+        dst_d = dst if same else torch.empty_like(src_d)
     else:
         dev = _core.require_cuda()
         src_d = t.contiguous().to(dev)

@@ -53,7 +53,12 @@ class BitrevPlan:
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.device(dev), torch.cuda.stream(side):
-            self._launch()  # warm: kernel attributes, occupancy caches, TMA encode paths
+            # warm: kernel attributes, occupancy caches, TMA encode paths.  An
+            # in-place plan warms with two launches: the permutation is an
+            # involution, so the caller's data comes back unchanged.
+            self._launch()
+            if dst is None:
+                self._launch()
         torch.cuda.current_stream(dev).wait_stream(side)
         torch.cuda.synchronize(dev)
         self.graph = torch.cuda.CUDAGraph()

@@ -199,9 +199,13 @@ def test_unpack_vector_and_generic_forms(cuda, E, g, bl):
 
 
 @pytest.mark.parametrize("E", [4, 8, 16])
-@pytest.mark.parametrize("bl,g,kb", [(14, 1, 0), (14, 1, 3), (16, 2, 2), (17, 3, 1), (20, 3, 4)])
+@pytest.mark.parametrize("bl,g,kb", [(14, 1, 0), (14, 1, 3), (14, 1, 7), (13, 1, 4), (16, 2, 2),
+                                      (17, 3, 1), (20, 3, 4)])
 def test_pack_layout(cuda, E, bl, g, kb):
-    """bitrev_sharded_pack: the local reversal laid out [c][d][k']."""
+    """bitrev_sharded_pack: the local reversal laid out [c][d][k'] -- through
+    the rectangular pack tiles, or the square scatter tiles when a sub-chunk
+    is shorter than a rectangular destination row (kb = 7) or the shard is
+    narrower than a rectangular tile (b_local = 13)."""
     dtype = {4: torch.int32, 8: torch.int64, 16: torch.complex128}[E]
     x = _random_bits(1 << bl, dtype, cuda)
     send = sharded._pack(x, bl, g, kb)

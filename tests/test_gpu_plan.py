@@ -84,3 +84,41 @@ def test_plan_validation(cuda):
         br.make_plan(x, 10, torch.zeros_like(x), stages=3)
     with pytest.raises(ValueError, match="CUDA"):
         br.make_plan(torch.zeros(1 << 10), 10)
+
+
+@pytest.mark.parametrize("replays", [1, 2, 3])
+def test_inplace_plan_leaves_data_untouched_until_replay(cuda, replays):
+    """Building an in-place plan must not permute the caller's array (its
+    warm-up runs the involution twice); a replay of k launches then applies
+    the permutation k times."""
+    b = 18
+    x = bits((1 << b,), torch.float64, cuda)
+    keep = x.clone()
+    plan = br.make_plan(x, b, replays_per_graph=replays)
+    torch.cuda.synchronize()
+    assert torch.equal(x.view(torch.uint8), keep.view(torch.uint8))
+    plan.replay()
+    torch.cuda.synchronize()
+    want = br.oracle_permute(keep, b) if replays % 2 else keep
+    assert torch.equal(x.view(torch.uint8), want.view(torch.uint8))
+
+
+def test_fft_prepass_out_on_another_device_kind(cuda):
+    """bitrev_dit_prepass with a CUDA input and a host (torch or numpy) or
+    strided `out`: the kernel writes a device temporary that is copied back,
+    never the foreign pointer."""
+    import numpy as np
+
+    b = 12
+    x = bits((4, 1 << b), torch.complex64, cuda)
+    want = br.bitrev_dit_prepass(x, b, 3)
+    host = torch.empty(x.shape, dtype=x.dtype)
+    br.bitrev_dit_prepass(x, b, 3, out=host)
+    assert torch.equal(host.view(torch.uint8), want.cpu().view(torch.uint8))
+    arr = np.empty((4, 1 << b), dtype=np.complex64)
+    br.bitrev_dit_prepass(x, b, 3, out=arr)
+    assert np.array_equal(arr.view(np.uint8), want.cpu().numpy().view(np.uint8))
+    wide = torch.empty((4, 2 << b), dtype=x.dtype, device=cuda)
+    view = wide[:, ::2]
+    br.bitrev_dit_prepass(x, b, 3, out=view)
+    assert torch.equal(view.contiguous().view(torch.uint8), want.view(torch.uint8))

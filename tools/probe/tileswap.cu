@@ -1,0 +1,142 @@
+// In-place DRAM access pattern probe (measurement only, not product code).
+//
+// Reproduces the global access pattern of the in-place tile-pair kernel WITHOUT
+// its shared-memory transposition: a work item is a pair of "tiles" {y, rev y};
+// each tile is ROWS rows of R contiguous bytes at stride STRIDE; both tiles are
+// read, then tile y's rows are written over tile rev(y)'s rows and vice versa.
+// Total footprint = ROWS * STRIDE bytes, the same as the real array.  Comparing
+// its GB/s with the real kernel on the same box separates the DRAM pattern
+// cost (run length R, visit order) from the kernel's own overheads.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tileswap tileswap.cu
+//   ./tileswap            (JSON lines)
+//
+// Orders of the pair list: 0 = ascending y, 1 = shuffled, 2 = "level" order
+// (the compact pair enumeration of the product kernel).
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <random>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint4 ldp(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+
+// CTA of NT threads per pair; each thread moves VPT vectors of each tile.
+template <int R, int ROWS, int NT>
+__global__ void __launch_bounds__(NT) tile_swap(char* a, const uint32_t* ys, int npairs, int m,
+                                               uint64_t stride) {
+  constexpr int CPR = R / 16;                 // 16-byte chunks per row
+  constexpr int VPT = ROWS * CPR / NT;        // chunks per thread per tile
+  static_assert(VPT >= 1 && ROWS * CPR % NT == 0, "split");
+  for (int p = blockIdx.x; p < npairs; p += gridDim.x) {
+    const uint64_t y = ys[p];
+    const uint64_t ry = m ? (__brevll(y) >> (64 - m)) : 0;
+    uint4 v0[VPT], v1[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int id = j * NT + threadIdx.x;
+      const int row = id / CPR, c = id % CPR;
+      v0[j] = ldp(a + row * stride + y * R + c * 16);
+      if (ry != y) v1[j] = ldp(a + row * stride + ry * R + c * 16);
+    }
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int id = j * NT + threadIdx.x;
+      const int row = id / CPR, c = id % CPR;
+      if (ry != y) {
+        stg(a + row * stride + ry * R + c * 16, v0[j]);
+        stg(a + row * stride + y * R + c * 16, v1[j]);
+      } else {
+        stg(a + row * stride + y * R + c * 16, v0[j]);
+      }
+    }
+  }
+}
+
+static uint32_t revb(uint32_t v, int m) {
+  uint32_t r = 0;
+  for (int i = 0; i < m; ++i) r |= ((v >> i) & 1u) << (m - 1 - i);
+  return r;
+}
+
+template <int R, int NT>
+void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
+  constexpr int ROWS = 64;
+  const uint64_t stride = total / ROWS;
+  int m = 0;
+  while (((uint64_t)R << (m + 1)) <= stride) ++m;
+  const uint64_t n = 1ull << m;
+  std::vector<uint32_t> asc;
+  for (uint32_t y = 0; y < n; ++y)
+    if (y <= revb(y, m)) asc.push_back(y);
+  std::vector<uint32_t> shuf = asc;
+  std::mt19937 g(1);
+  std::shuffle(shuf.begin(), shuf.end(), g);
+  // level order: by the position of the first mirrored-bit mismatch
+  std::vector<uint32_t> lvl = asc;
+  std::stable_sort(lvl.begin(), lvl.end(), [&](uint32_t x, uint32_t y) {
+    auto level = [&](uint32_t v) {
+      for (int k = 0; k < m / 2; ++k)
+        if (((v >> k) & 1) != ((v >> (m - 1 - k)) & 1)) return k;
+      return m;
+    };
+    return level(x) < level(y);
+  });
+  const std::vector<uint32_t>* orders[3] = {&asc, &shuf, &lvl};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int o = 0; o < 3; ++o) {
+    cudaMemcpy(d_ys, orders[o]->data(), orders[o]->size() * 4, cudaMemcpyHostToDevice);
+    const int np = (int)orders[o]->size();
+    const int grid = sms * ctas_per_sm;
+    for (int w = 0; w < 3; ++w) tile_swap<R, ROWS, NT><<<grid, NT>>>(a, d_ys, np, m, stride);
+    std::vector<float> ts;
+    for (int r = 0; r < 15; ++r) {
+      cudaEventRecord(e0);
+      tile_swap<R, ROWS, NT><<<grid, NT>>>(a, d_ys, np, m, stride);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts.push_back(ms);
+    }
+    std::sort(ts.begin(), ts.end());
+    const uint64_t moved = 2 * (uint64_t)ROWS * R * n;
+    printf("{\"bytes\": %llu, \"R\": %d, \"m\": %d, \"order\": %d, \"nt\": %d, \"ctas_per_sm\": %d, "
+           "\"gbs\": %.1f, \"best_gbs\": %.1f}\n",
+           (unsigned long long)total, R, m, o, NT, ctas_per_sm, moved / ts[ts.size() / 2] / 1e6,
+           moved / ts[0] / 1e6);
+  }
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (uint64_t total : {512ull << 20, 4096ull << 20}) {
+    char* a;
+    uint32_t* ys;
+    cudaMalloc(&a, total);
+    cudaMalloc(&ys, (total / 64 / 256) * 4 + 1024);
+    cudaMemset(a, 3, total);
+    run<256, 256>(a, ys, total, sms, 4);
+    run<512, 256>(a, ys, total, sms, 4);
+    run<512, 512>(a, ys, total, sms, 2);
+    run<1024, 512>(a, ys, total, sms, 2);
+    cudaFree(a);
+    cudaFree(ys);
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("{\"status\": \"%s\"}\n", cudaGetErrorString(e));
+  return 0;
+}
