@@ -842,7 +842,25 @@ int launch_scatter(const void* local, char* const* peer, int b_local, int g, int
 cudaStream_t st_of(void* stream) { return static_cast<cudaStream_t>(stream); }
 
 template <int E, int QX, int QZ>
-int launch_pack_rect(const void* src, void* dst, int b, int g, int sb, cudaStream_t st) {
+int launch_pack_rect(const void* src, char* const* peer, int rank, int b, int g, int sb,
+                     cudaStream_t st);
+
+// Rectangular pack tiles per element size (1 KB destination rows): E=4
+// (8,6), E=8 (7,5), E=16 (6,6); BITREV_ETILE when the shape does not fit.
+int dispatch_pack_rect(int E, const void* src, char* const* peer, int rank, int b, int g, int sb,
+                       cudaStream_t st) {
+  if (!aligned16(src)) return BITREV_ETILE;
+  for (int d = 0; d < (1 << g); ++d)
+    if (!aligned16(peer[d])) return BITREV_ETILE;
+  if (E == 4) return launch_pack_rect<4, 8, 6>(src, peer, rank, b, g, sb, st);
+  if (E == 8) return launch_pack_rect<8, 7, 5>(src, peer, rank, b, g, sb, st);
+  if (E == 16) return launch_pack_rect<16, 6, 6>(src, peer, rank, b, g, sb, st);
+  return BITREV_ETILE;
+}
+
+template <int E, int QX, int QZ>
+int launch_pack_rect(const void* src, char* const* peer, int rank, int b, int g, int sb,
+                     cudaStream_t st) {
   using T = Rect<E, QX, QZ>;
   if (b < QX + QZ || sb < QX) return BITREV_ETILE;
   auto kern = bitrev_pack_rect_kernel<E, QX, QZ>;
@@ -851,13 +869,14 @@ int launch_pack_rect(const void* src, void* dst, int b, int g, int sb, cudaStrea
   memset(&pa, 0, sizeof pa);
   TileArgs& a = pa.t;
   a.src = static_cast<const char*>(src);
-  a.dst = static_cast<char*>(dst);
   a.b = b;
   a.m = b - QX - QZ;
   a.ntiles = 1ull << a.m;
   a.batch = 1;
+  for (int d = 0; d < (1 << g); ++d) pa.peer[d] = peer[d];
   pa.g = g;
   pa.sb = sb;
+  pa.rank = rank;
   kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(pa);
   return finish_launch();
 }
@@ -1374,9 +1393,13 @@ int bitrev_sharded_scatter(const void* local, void* const* peer_recv, int b_loca
   if (!local || !peer_recv) return BITREV_ENULL;
   if (b_local < 2 * g) return BITREV_ESHARD;
   char* peer[kMaxPeers] = {};
-  for (int d = 0; d < (1 << g); ++d) peer[d] = static_cast<char*>(peer_recv[d]);
-  return launch_scatter(local, peer, b_local, g, rank, b_local - g, E,
-                        static_cast<cudaStream_t>(stream));
+  for (int d = 0; d < (1 << g); ++d) {
+    if (!peer_recv[d]) return BITREV_ENULL;
+    peer[d] = static_cast<char*>(peer_recv[d]);
+  }
+  const int rc = dispatch_pack_rect(E, local, peer, rank, b_local, g, b_local - g, st_of(stream));
+  if (rc != BITREV_ETILE) return rc;
+  return launch_scatter(local, peer, b_local, g, rank, b_local - g, E, st_of(stream));
 }
 
 int bitrev_sharded_pack(const void* local, void* send, int b_local, int g, int chunk_bits,
@@ -1393,17 +1416,13 @@ int bitrev_sharded_pack(const void* local, void* send, int b_local, int g, int c
   if (chunk_bits == 0)  // one chunk: the send layout is the plain reversal
     return bitrev_oop(local, send, b_local, E, 1, 0, 0, stream);
   const int sb = b_local - g - chunk_bits;
-  if (aligned16(local) && aligned16(send)) {
-    // rectangular tiles with re-addressed rows (1 KB destination rows)
-    int rc = BITREV_ETILE;
-    if (E == 4) rc = launch_pack_rect<4, 8, 6>(local, send, b_local, g, sb, st_of(stream));
-    if (E == 8) rc = launch_pack_rect<8, 7, 5>(local, send, b_local, g, sb, st_of(stream));
-    if (E == 16) rc = launch_pack_rect<16, 6, 6>(local, send, b_local, g, sb, st_of(stream));
-    if (rc != BITREV_ETILE) return rc;
-  }
   char* peer[kMaxPeers] = {};
   for (int d = 0; d < (1 << g); ++d) peer[d] = static_cast<char*>(send) + ((uint64_t)E << sb) * d;
-  return launch_scatter(local, peer, b_local, g, 0, sb, E, static_cast<cudaStream_t>(stream));
+  // rectangular tiles with re-addressed rows (1 KB destination rows), else
+  // the square scatter tiles (shorter rows fit shorter sub-chunks)
+  const int rc = dispatch_pack_rect(E, local, peer, 0, b_local, g, sb, st_of(stream));
+  if (rc != BITREV_ETILE) return rc;
+  return launch_scatter(local, peer, b_local, g, 0, sb, E, st_of(stream));
 }
 
 int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int elem_bytes,

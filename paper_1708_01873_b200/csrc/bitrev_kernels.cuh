@@ -486,18 +486,26 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
 }
 
 // ---------------------------------------------------------------------------
-// sharded plan, step 1 for an all-to-all in K = 2^kb rounds: the rectangular
-// tile kernel above with its destination rows re-addressed.  Local output
-// index u = d * C + c * S + k' (d = destination rank, c = round, S = 2^sb)
-// is stored at u' = c * G * S + d * S + k', so that round c's send data is
-// the contiguous slice [c * G * S, (c + 1) * G * S) with equal per-rank
-// splits.  A destination row (2^QX contiguous u) never straddles a
-// sub-chunk (S >= 2^QX), so the remap costs a few integer ops per row.
+// sharded plan, step 1 (and 1+2 fused): the rectangular tile kernel above
+// with its destination rows re-addressed.  Local output index
+// u = d * C + c * S + k' (d = destination rank, c = exchange round, S = 2^sb)
+// is stored at peer[d] + (c * G * S + rank * S + k') * E.
+//   pack    (all-to-all in K = C / S rounds): peer[d] = send + d * S * E,
+//           rank = 0, so round c's send data is the contiguous slice
+//           [c * G * S, (c + 1) * G * S) with equal per-rank splits;
+//   scatter (peer-mapped receive buffers): peer[d] = rank d's buffer, S = C,
+//           so the row lands where the all-to-all would have put it.
+// A destination row (2^QX contiguous u) never straddles a sub-chunk
+// (S >= 2^QX), so the remap costs a few integer ops per row.
+
+constexpr int kMaxPeers = 8;
 
 struct PackArgs {
   TileArgs t;
-  int g;   // log2 G
-  int sb;  // log2 S
+  char* peer[kMaxPeers];  // base of destination rank d's region
+  int g;                  // log2 G
+  int sb;                 // log2 S
+  int rank;               // this rank's slot inside each destination region
 };
 
 template <int E, int QX, int QZ>
@@ -550,8 +558,9 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
       const int col = id % T::GX, z = id / T::GX;
       const uint64_t u = ((uint64_t)(__brev((unsigned)z) >> (32 - QZ)) << (a.b - QZ)) | ry;
       const uint64_t rest = u & cmask;
-      const uint64_t up = ((rest >> pa.sb) << (pa.sb + pa.g)) | ((u >> db) << pa.sb) | (rest & smask);
-      st_vec<true>(a.dst + up * E + (uint64_t)col * 16, smem[sidx(z, col)]);
+      const uint64_t off = ((rest >> pa.sb) << (pa.sb + pa.g)) | ((uint64_t)pa.rank << pa.sb) |
+                           (rest & smask);
+      st_vec<true>(pa.peer[u >> db] + off * E + (uint64_t)col * 16, smem[sidx(z, col)]);
     }
     if (tn >= a.ntiles) break;
     __syncthreads();
@@ -570,8 +579,6 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
 // pointers mapped over NVLink/NVSwitch (symmetric memory / CUDA IPC) the row
 // stores go straight into the peers' HBM -- no send buffer, no separate
 // all-to-all pass.  On one device the same kernel runs with G local buffers.
-
-constexpr int kMaxPeers = 8;
 
 struct ScatterArgs {
   TileArgs t;

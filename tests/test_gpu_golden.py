@@ -217,10 +217,12 @@ def test_sentinel_64bit_sizes(cuda, b, inplace):
 
 @pytest.mark.parametrize("b,G,dtype", [(16, 2, torch.int64), (18, 4, torch.float32),
                                        (20, 8, torch.complex128), (26, 8, torch.complex64),
-                                       (24, 8, torch.int32)])
+                                       (24, 8, torch.int32), (14, 2, torch.int32)])
 def test_sharded_p2p_scatter_kernel(cuda, b, G, dtype):
     """Fused local-reversal + scatter into the peers' receive buffers
-    (bitrev_sharded_scatter), all ranks emulated on one device."""
+    (bitrev_sharded_scatter: rectangular tiles, or square tiles for a shard
+    narrower than a rectangular tile, b = 14 float32), all ranks emulated on
+    one device."""
     x = torch.empty((1 << b) * torch.empty(0, dtype=dtype).element_size(), dtype=torch.uint8,
                     device=cuda).random_(0, 256).view(dtype)
     got = torch.cat(sharded.emulate_sharded_p2p(x, b, G))

@@ -46,6 +46,18 @@ __global__ void __launch_bounds__(256) copy_lin(const uint4* s, uint4* d, uint64
   for (; i < nv; i += stride) stg(d + i, ldg(s + i));
 }
 
+// each CTA copies one contiguous chunk of nv / gridDim vectors
+__global__ void __launch_bounds__(256) copy_chunk(const uint4* s, uint4* d, uint64_t nv) {
+  const uint64_t per = nv / gridDim.x;
+  const uint64_t lo = blockIdx.x * per, hi = lo + per;
+  uint64_t i = lo + threadIdx.x;
+  for (; i + 3 * 256 < hi; i += 4 * 256) {
+    uint4 a = ldg(s + i), b = ldg(s + i + 256), c = ldg(s + i + 512), e = ldg(s + i + 768);
+    stg(d + i, a); stg(d + i + 256, b); stg(d + i + 512, c); stg(d + i + 768, e);
+  }
+  for (; i < hi; i += 256) stg(d + i, ldg(s + i));
+}
+
 // MODE 0: dst rev(k) <- src k; MODE 1: dst (k*A mod nb) <- src k
 template <int R, int U, int MODE>
 __global__ void __launch_bounds__(256) blk_oop(const char* s, char* d, int lb) {
@@ -164,6 +176,16 @@ int main() {
     for (int cps : {4, 8}) {
       double t = time_ms([&] { copy_lin<<<sms * cps, 256>>>((const uint4*)s, (uint4*)d, nv); }, 15);
       printf("{\"bytes\": %llu, \"copy_ctas_per_sm\": %d, \"copy_gbs\": %.1f}\n",
+             (unsigned long long)bytes, cps, 2.0 * bytes / t / 1e6);
+    }
+    {
+      double t = time_ms([&] { cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice); }, 15);
+      printf("{\"bytes\": %llu, \"memcpy_d2d_gbs\": %.1f}\n", (unsigned long long)bytes,
+             2.0 * bytes / t / 1e6);
+    }
+    for (int cps : {1, 2, 4, 8}) {
+      double t = time_ms([&] { copy_chunk<<<sms * cps, 256>>>((const uint4*)s, (uint4*)d, nv); }, 15);
+      printf("{\"bytes\": %llu, \"chunk_ctas_per_sm\": %d, \"chunk_copy_gbs\": %.1f}\n",
              (unsigned long long)bytes, cps, 2.0 * bytes / t / 1e6);
     }
     run_r<256, 4>(s, d, bytes, sms, 8);
