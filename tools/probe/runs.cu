@@ -46,6 +46,143 @@ __global__ void __launch_bounds__(256) copy_lin(const uint4* s, uint4* d, uint64
   for (; i < nv; i += stride) stg(d + i, ldg(s + i));
 }
 
+__device__ __forceinline__ uint4 ldg_pf(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_cs(void* p, const uint4& v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+// MODE 1: streaming stores; MODE 2: L2 256-byte prefetch on loads; MODE 3: both
+template <int MODE>
+__global__ void __launch_bounds__(256) copy_var(const uint4* s, uint4* d, uint64_t nv) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  auto ld = [&](const uint4* p) { return (MODE & 2) ? ldg_pf(p) : ldg(p); };
+  auto st = [&](uint4* p, const uint4& v) { if (MODE & 1) stg_cs(p, v); else stg(p, v); };
+  for (; i + 3 * stride < nv; i += 4 * stride) {
+    uint4 a = ld(s + i), b = ld(s + i + stride), c = ld(s + i + 2 * stride), e = ld(s + i + 3 * stride);
+    st(d + i, a); st(d + i + stride, b); st(d + i + 2 * stride, c); st(d + i + 3 * stride, e);
+  }
+  for (; i < nv; i += stride) st(d + i, ld(s + i));
+}
+
+// TMA bulk copy: grid-stride over CH-byte chunks, each staged g2s then s2g
+// (two smem slots, bulk groups); chunk order globally sequential
+template <int CH>
+__global__ void __launch_bounds__(32) copy_bulk(const char* s, char* d, uint64_t bytes) {
+  __shared__ __align__(128) unsigned char buf[2][CH];
+  __shared__ __align__(8) unsigned long long bar[2];
+  const uint32_t b0 = (uint32_t)__cvta_generic_to_shared(&bar[0]);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b0 + 8));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const uint64_t nch = bytes / CH;
+  int k = 0;
+  uint32_t phase[2] = {0, 0};
+  for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x, ++k) {
+    const int slot = k & 1;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(buf[slot]);
+    const uint32_t bb = b0 + 8 * slot;
+    // the slot's previous store must have read shared memory
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(CH) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sb), "l"(s + c * CH), "r"(CH), "r"(bb) : "memory");
+    asm volatile("{\n.reg .pred p;\nW%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W%=;\n}"
+                 ::"r"(bb), "r"(phase[slot]) : "memory");
+    phase[slot] ^= 1;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d + c * CH), "r"(sb), "r"(CH) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <typename F>
+double time_ms(F f, int reps);
+
+// TMA bulk permutation of R-byte blocks, one elected thread per CTA, NS slots:
+// SWAP = false: dst block rev(k) <- src block k  (unit = one block)
+// SWAP = true : in place, blocks k <-> rev(k), k <= rev(k)  (unit = the pair)
+template <int R, int NS, bool SWAP>
+__global__ void __launch_bounds__(32) bulk_perm(const char* s, char* d, int lb) {
+  constexpr int UB = SWAP ? 2 * R : R;  // bytes per unit
+  __shared__ __align__(128) unsigned char buf[NS][UB];
+  __shared__ __align__(8) unsigned long long bar[NS];
+  if (threadIdx.x != 0) return;
+  const uint32_t b0 = (uint32_t)__cvta_generic_to_shared(&bar[0]);
+  for (int i = 0; i < NS; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b0 + 8 * i));
+  asm volatile("fence.mbarrier_init.release.cluster;");
+  const uint64_t nb = 1ull << lb;
+  // unit list of this CTA: k = blockIdx.x + j * gridDim.x (skipping k > rev k when SWAP)
+  auto unit_k = [&](uint64_t j, uint64_t& k) {
+    k = blockIdx.x + j * gridDim.x;
+    return k < nb;
+  };
+  uint32_t phase[NS] = {};
+  auto issue_load = [&](uint64_t j) {
+    uint64_t k;
+    if (!unit_k(j, k)) return;
+    const int slot = (int)(j % NS);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(buf[slot]);
+    const uint32_t bb = b0 + 8 * slot;
+    const uint64_t r = rev(k, lb);
+    const bool act = !SWAP || k <= r;
+    const uint32_t bytes = act ? (SWAP ? (k == r ? R : 2 * R) : R) : 0;
+    if (!bytes) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bb) : "memory"); return; }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sb), "l"(s + k * R), "r"(R), "r"(bb) : "memory");
+    if (SWAP && k != r)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(sb + R), "l"(s + r * R), "r"(R), "r"(bb) : "memory");
+  };
+  for (int j = 0; j < NS - 1; ++j) issue_load(j);
+  for (uint64_t j = 0;; ++j) {
+    uint64_t k;
+    if (!unit_k(j, k)) break;
+    // slot of unit j+NS-1 was last used by unit j-1: its stores must have read smem
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    issue_load(j + NS - 1);
+    const int slot = (int)(j % NS);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(buf[slot]);
+    const uint32_t bb = b0 + 8 * slot;
+    asm volatile("{\n.reg .pred p;\nW%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W%=;\n}"
+                 ::"r"(bb), "r"(phase[slot]) : "memory");
+    phase[slot] ^= 1;
+    const uint64_t r = rev(k, lb);
+    if (!SWAP) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d + r * R), "r"(sb), "r"(R) : "memory");
+    } else if (k <= r) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d + r * R), "r"(sb), "r"(R) : "memory");
+      if (k != r)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d + k * R), "r"(sb + R), "r"(R) : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int R, int NS>
+void run_bulk(char* s, char* d, uint64_t bytes, int sms, int cps) {
+  int lb = 0;
+  while ((uint64_t(R) << (lb + 1)) <= bytes) ++lb;
+  const uint64_t used = uint64_t(R) << lb;
+  const int grid = sms * cps;
+  double t0 = time_ms([&] { bulk_perm<R, NS, false><<<grid, 32>>>(s, d, lb); }, 15);
+  double t1 = time_ms([&] { bulk_perm<R, NS, true><<<grid, 32>>>(d, d, lb); }, 15);
+  printf("{\"bytes\": %llu, \"R\": %d, \"NS\": %d, \"cps\": %d, \"bulk_oop_rev_gbs\": %.1f, "
+         "\"bulk_swap_rev_gbs\": %.1f}\n",
+         (unsigned long long)used, R, NS, cps, 2.0 * used / t0 / 1e6, 2.0 * used / t1 / 1e6);
+}
+
 // each CTA copies one contiguous chunk of nv / gridDim vectors
 __global__ void __launch_bounds__(256) copy_chunk(const uint4* s, uint4* d, uint64_t nv) {
   const uint64_t per = nv / gridDim.x;
@@ -183,11 +320,29 @@ int main() {
       printf("{\"bytes\": %llu, \"memcpy_d2d_gbs\": %.1f}\n", (unsigned long long)bytes,
              2.0 * bytes / t / 1e6);
     }
-    for (int cps : {1, 2, 4, 8}) {
+    {
+      double t1 = time_ms([&] { copy_var<1><<<sms * 4, 256>>>((const uint4*)s, (uint4*)d, nv); }, 15);
+      double t2 = time_ms([&] { copy_var<2><<<sms * 4, 256>>>((const uint4*)s, (uint4*)d, nv); }, 15);
+      double t3 = time_ms([&] { copy_var<3><<<sms * 4, 256>>>((const uint4*)s, (uint4*)d, nv); }, 15);
+      double t4 = time_ms([&] { copy_bulk<16384><<<sms * 8, 32>>>(s, d, bytes); }, 15);
+      double t5 = time_ms([&] { copy_bulk<8192><<<sms * 16, 32>>>(s, d, bytes); }, 15);
+      double t6 = time_ms([&] { copy_bulk<4096><<<sms * 24, 32>>>(s, d, bytes); }, 15);
+      printf("{\"bytes\": %llu, \"copy_cs_gbs\": %.1f, \"copy_l2pf_gbs\": %.1f, \"copy_cs_l2pf_gbs\": %.1f, "
+             "\"bulk16k_gbs\": %.1f, \"bulk8k_gbs\": %.1f, \"bulk4k_gbs\": %.1f}\n",
+             (unsigned long long)bytes, 2.0 * bytes / t1 / 1e6, 2.0 * bytes / t2 / 1e6,
+             2.0 * bytes / t3 / 1e6, 2.0 * bytes / t4 / 1e6, 2.0 * bytes / t5 / 1e6,
+             2.0 * bytes / t6 / 1e6);
+    }
+    for (int cps : {2, 8}) {
       double t = time_ms([&] { copy_chunk<<<sms * cps, 256>>>((const uint4*)s, (uint4*)d, nv); }, 15);
       printf("{\"bytes\": %llu, \"chunk_ctas_per_sm\": %d, \"chunk_copy_gbs\": %.1f}\n",
              (unsigned long long)bytes, cps, 2.0 * bytes / t / 1e6);
     }
+    run_bulk<512, 4>(s, d, bytes, sms, 16);
+    run_bulk<512, 8>(s, d, bytes, sms, 16);
+    run_bulk<1024, 4>(s, d, bytes, sms, 16);
+    run_bulk<2048, 4>(s, d, bytes, sms, 8);
+    run_bulk<4096, 4>(s, d, bytes, sms, 4);
     run_r<256, 4>(s, d, bytes, sms, 8);
     run_r<512, 4>(s, d, bytes, sms, 8);
     run_r<1024, 2>(s, d, bytes, sms, 8);
