@@ -1353,7 +1353,16 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   // (16 rows: +29 % at 4 stages); complex64 with QZ = 5 needs ~170 registers
   // (1 CTA/SM) and trails QZ = 4 once the drain's shared-memory conflicts are
   // gone.
-  const int qx = E == 8 ? 7 : 6, qz = 4;
+  // complex64: 256-byte source pieces (QZ = 5, 32 KB tiles, 2 CTAs/SM) for 2-6
+  // fused stages, 128-byte pieces (QZ = 4, 3 CTAs/SM) for 1 and 7: measured
+  // A/B (profiles/r02_fft_qz_ab.txt): QZ = 5 +1 % / +3 % / +3 % / +5 % / +7 %
+  // at 2 / 3 / 4 / 5 / 6 stages, -0.4 % at 1 stage, -2 % at 7 (the third
+  // layout exchange tips it into issue-bound).  BITREV_B200_FFT_QZ=4|5 forces
+  // one shape (A/B runs).
+  static const int qz_env = env_int("BITREV_B200_FFT_QZ", 0);
+  const int qx = E == 8 ? 7 : 6;
+  int qz = 4;
+  if (E == 8) qz = qz_env == 4 || qz_env == 5 ? qz_env : (stages >= 2 && stages <= 6 ? 5 : 4);
   if (stages > qx || b < qx + qz) return BITREV_ESTAGES;
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
@@ -1368,7 +1377,13 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                      \
     return finish_launch();                                                                  \
   }
-  if (E == 8) {
+  if (E == 8 && qz == 5) {
+    switch (stages) {
+      FFT_LAUNCH(8, 7, 5, 1) FFT_LAUNCH(8, 7, 5, 2) FFT_LAUNCH(8, 7, 5, 3)
+      FFT_LAUNCH(8, 7, 5, 4) FFT_LAUNCH(8, 7, 5, 5) FFT_LAUNCH(8, 7, 5, 6)
+      FFT_LAUNCH(8, 7, 5, 7)
+    }
+  } else if (E == 8) {
     switch (stages) {
       FFT_LAUNCH(8, 7, 4, 1) FFT_LAUNCH(8, 7, 4, 2) FFT_LAUNCH(8, 7, 4, 3)
       FFT_LAUNCH(8, 7, 4, 4) FFT_LAUNCH(8, 7, 4, 5) FFT_LAUNCH(8, 7, 4, 6)

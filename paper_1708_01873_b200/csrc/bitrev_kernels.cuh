@@ -1396,11 +1396,17 @@ __device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_
   constexpr int V = T::V, LPR = (1 << QX) / 4, RPP = 32 / LPR;
   constexpr int NWARPS = T::THREADS / 32;
   constexpr int ROWS = 1 << QZ;
-  constexpr int NR = (ROWS + NWARPS * RPP - 1) / (NWARPS * RPP);
+  constexpr int NRT = (ROWS + NWARPS * RPP - 1) / (NWARPS * RPP);  // rows per lane
+  // rows are drained in groups of NR: every group runs load -> stages ->
+  // store on its own, so the registers of one group's row data are reused by
+  // the next (taller tiles do not cost registers)
+  constexpr int NR = NRT < 2 ? NRT : 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp * RPP >= ROWS) return;
   const int h = lane / LPR, ll = lane % LPR;
-  auto row_of = [&](int i) { return (warp + i * NWARPS) * RPP + h; };
+#pragma unroll 1
+  for (int grp = 0; grp < NRT / NR; ++grp) {
+  auto row_of = [&](int i) { return (warp + (grp * NR + i) * NWARPS) * RPP + h; };
   auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
   const C w4 = inverse ? C{0, 1} : C{0, -1};
   C v[NR][4];
@@ -1551,11 +1557,13 @@ __device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_
   constexpr int LF = stages <= 2 ? 0 : stages <= 4 ? (kBtoC ? 2 : 1) : stages <= 6 ? 2 : 3;
   store(std::integral_constant<int, LF>{});
   (void)L;
+  }
 }
 
 // Rectangular-tile FFT pre-pass (bitrev_oop_rect_kernel's load/stage path).
 template <int E, int QX, int QZ, int STAGES>
-__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS, STAGES >= BITREV_FFT_MINB_FROM ? BITREV_FFT_MINB : 1)
+__global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
+                                  STAGES >= BITREV_FFT_MINB_FROM ? (QZ >= 5 ? 2 : BITREV_FFT_MINB) : 1)
     bitrev_fft_rect_kernel(FftArgs fa) {
   using T = Rect<E, QX, QZ>;
   using C = typename Cplx<E>::T;
