@@ -1362,7 +1362,7 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   static const int qz_env = env_int("BITREV_B200_FFT_QZ", 0);
   const int qx = E == 8 ? 7 : 6;
   int qz = 4;
-  if (E == 8) qz = qz_env == 4 || qz_env == 5 ? qz_env : (stages >= 2 && stages <= 6 ? 5 : 4);
+  if (E == 8) qz = qz_env == 4 || qz_env == 5 ? qz_env : (stages >= 2 ? 5 : 4);
   if (stages > qx || b < qx + qz) return BITREV_ESTAGES;
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);

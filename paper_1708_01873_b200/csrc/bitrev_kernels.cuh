@@ -69,6 +69,9 @@
 #ifndef BITREV_RING_BUDGET_KB
 #define BITREV_RING_BUDGET_KB 96  // TMA ring bytes per CTA (96 KB -> 2 CTAs/SM)
 #endif
+#ifndef BITREV_FFT_R8_FROM
+#define BITREV_FFT_R8_FROM 7  // complex64: radix-8 drain from this many fused stages (4..8; 8 = never)
+#endif
 #ifndef BITREV_MINB_IP
 #define BITREV_MINB_IP 1  // __launch_bounds__ min CTAs/SM, in-place tile kernel
 #endif
@@ -1560,6 +1563,159 @@ __device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_
   }
 }
 
+// Radix-8 drain for complex64 rows of 128 (QX = 7), 4-7 fused stages.  The
+// radix-4 drain above needs three layout exchanges for 7 stages (A -> B -> C
+// -> D); here a lane holds 8 elements and 16 lanes share a row (two rows per
+// warp pass), so three stages run per in-register pass and two exchanges do:
+//   A8: x' = 8 ll + m                        stages 1-3 (twiddles: constants)
+//   B8: x' = (ll & 7) + 8 m + 64 (ll >> 3)    stages 4-6
+//   C8: x' = ll + 16 m                        stage 7, then a natural store
+// (ll < 16 = lane within the row, m < 8 = register slot).  The exchanges go
+// through the half-warp's own row of the tile buffer with the 8-byte-slot
+// swizzle f(x) = x ^ (x >> 4 & 7) ^ ((x >> 6 & 1) << 3), under which each
+// layout's 16 lanes of a row hit 16 distinct bank slots.
+struct LaneTw8 {
+  float2 w16, w32, w64, w128;  // W_16^r, W_32^r, W_64^r (r = ll & 7), W_128^ll
+  __device__ __forceinline__ void load(const float2* tw, int ll) {  // tw = W_128^j, j < 64
+    const int r = ll & 7;
+    w16 = tw[r << 3];
+    w32 = tw[r << 2];
+    w64 = tw[r << 1];
+    w128 = tw[ll];
+  }
+};
+
+__device__ __forceinline__ int fft8_swz(int x) { return x ^ ((x >> 4) & 7) ^ (((x >> 6) & 1) << 3); }
+
+template <int QZ, int STAGES>
+__device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_t dst_row,
+                                                  const LaneTw8& lt, bool inverse) {
+  static_assert(STAGES >= 4 && STAGES <= 7, "radix-8 drain: 4 to 7 stages");
+  using C = float2;
+  using T = Rect<8, 7, QZ>;
+  constexpr int NWARPS = T::THREADS / 32;
+  constexpr int ROWS = 1 << QZ;
+  constexpr int PASSES = ROWS / (2 * NWARPS);
+  static_assert(PASSES >= 1 && ROWS % (2 * NWARPS) == 0, "two rows per warp pass");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = lane >> 4, ll = lane & 15;
+  auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
+  const float sg = inverse ? 1.f : -1.f;          // sign of the twiddle exponent
+  const float rh = 0.70710678118654752f;
+  const C w4 = C{0.f, sg};                          // W_4
+  const C w8 = C{rh, sg * rh};                      // W_8
+  const C w83 = C{-rh, sg * rh};                    // W_8^3
+  auto mulj = [&](C a) { return C{-sg * a.y, sg * a.x}; };  // a * W_4
+#pragma unroll 1
+  for (int pass = 0; pass < PASSES; ++pass) {
+    const int z = (warp + pass * NWARPS) * 2 + h;
+    C v[8];
+    // A8 from the staged tile: the lane's 4 chunks 4 ll + c, read from a
+    // rotated start so the 8 lanes of a quarter warp cover all 8 bank slots
+    {
+      const int rot = (ll >> 1) & 3;
+      uint4 q[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) q[c] = U[sidx(z, 4 * ll + ((c + rot) & 3))];
+      if (rot & 1) {
+        const uint4 t = q[3];
+        q[3] = q[2];
+        q[2] = q[1];
+        q[1] = q[0];
+        q[0] = t;
+      }
+      if (rot & 2) {
+        uint4 t = q[0];
+        q[0] = q[2];
+        q[2] = t;
+        t = q[1];
+        q[1] = q[3];
+        q[3] = t;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        v[2 * c] = make_float2(__uint_as_float(q[c].x), __uint_as_float(q[c].y));
+        v[2 * c + 1] = make_float2(__uint_as_float(q[c].z), __uint_as_float(q[c].w));
+      }
+    }
+    // stages 1-3 (A8): constant twiddles
+#pragma unroll
+    for (int m = 0; m < 8; m += 2) {
+      const C t = v[m + 1];
+      v[m + 1] = csub(v[m], t);
+      v[m] = cadd(v[m], t);
+    }
+#pragma unroll
+    for (int g = 0; g < 8; g += 4) {
+      C t = v[g + 2];
+      v[g + 2] = csub(v[g], t);
+      v[g] = cadd(v[g], t);
+      t = mulj(v[g + 3]);
+      v[g + 3] = csub(v[g + 1], t);
+      v[g + 1] = cadd(v[g + 1], t);
+    }
+    {
+      C t = v[4];
+      v[4] = csub(v[0], t);
+      v[0] = cadd(v[0], t);
+      t = cmul(v[5], w8);
+      v[5] = csub(v[1], t);
+      v[1] = cadd(v[1], t);
+      t = mulj(v[6]);
+      v[6] = csub(v[2], t);
+      v[2] = cadd(v[2], t);
+      t = cmul(v[7], w83);
+      v[7] = csub(v[3], t);
+      v[3] = cadd(v[3], t);
+    }
+    C* row = reinterpret_cast<C*>(U) + (size_t)z * 128;
+    __syncwarp();  // every lane of the row has read its staged chunks
+#pragma unroll
+    for (int m = 0; m < 8; ++m) row[fft8_swz(8 * ll + m)] = v[m];
+    __syncwarp();
+    const int r = ll & 7, hi = ll >> 3;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) v[m] = row[fft8_swz(r + 8 * m + 64 * hi)];
+    // stages 4-6 (B8): pairs 8, 16, 32 apart
+#pragma unroll
+    for (int m = 0; m < 8; m += 2) bfly(v[m], v[m + 1], lt.w16);
+    if constexpr (STAGES >= 5) {
+      const C a = lt.w32, b = mulj(lt.w32);  // W_32^r, W_32^(r+8)
+#pragma unroll
+      for (int g = 0; g < 8; g += 4) {
+        bfly(v[g], v[g + 2], a);
+        bfly(v[g + 1], v[g + 3], b);
+      }
+    }
+    if constexpr (STAGES >= 6) {
+      const C a0 = lt.w64, a1 = cmul(lt.w64, w8), a2 = mulj(lt.w64), a3 = cmul(lt.w64, w83);
+      bfly(v[0], v[4], a0);
+      bfly(v[1], v[5], a1);
+      bfly(v[2], v[6], a2);
+      bfly(v[3], v[7], a3);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 8; ++m) row[fft8_swz(r + 8 * m + 64 * hi)] = v[m];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 8; ++m) v[m] = row[fft8_swz(ll + 16 * m)];
+    // stage 7 (C8): pairs 64 apart, W_128^(ll + 16 t) = W_128^ll * W_8^t
+    if constexpr (STAGES >= 7) {
+      const C b0 = lt.w128, b1 = cmul(lt.w128, w8), b2 = mulj(lt.w128), b3 = cmul(lt.w128, w83);
+      bfly(v[0], v[4], b0);
+      bfly(v[1], v[5], b1);
+      bfly(v[2], v[6], b2);
+      bfly(v[3], v[7], b3);
+    }
+    // natural store: for each m the row's 16 lanes write 128 contiguous bytes
+    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - QZ)) * dst_row;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) *reinterpret_cast<C*>(drow + (uint64_t)(ll + 16 * m) * 8) = v[m];
+    __syncwarp();  // the row is free for the next pass's exchange
+  }
+}
+
 // Rectangular-tile FFT pre-pass (bitrev_oop_rect_kernel's load/stage path).
 template <int E, int QX, int QZ, int STAGES>
 __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
@@ -1598,8 +1754,11 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
   if (t >= a.ntiles) return;
   load(t);
   __syncthreads();  // publish twq
-  LaneTw<E, QX, STAGES> lt;
-  lt.load(twq, (threadIdx.x & 31) % ((1 << QX) / 4));
+  constexpr bool kR8 = E == 8 && QX == 7 && STAGES >= BITREV_FFT_R8_FROM && STAGES >= 4;
+  LaneTw<E, QX, kR8 ? 0 : STAGES> lt;
+  LaneTw8 lt8;
+  if constexpr (kR8) lt8.load(reinterpret_cast<const float2*>(twq), threadIdx.x & 15);
+  else lt.load(twq, (threadIdx.x & 31) % ((1 << QX) / 4));
   for (;;) {
     const uint64_t bi = t >> a.m, y = t & mmask;
 #pragma unroll
@@ -1614,7 +1773,8 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) load(tn);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
-    fft_rows_drain_r4<E, QX, QZ, STAGES>(smem, dbase, dst_row, lt, fa.inverse != 0);
+    if constexpr (kR8) fft_rows_drain_r8<QZ, STAGES>(smem, dbase, dst_row, lt8, fa.inverse != 0);
+    else fft_rows_drain_r4<E, QX, QZ, STAGES>(smem, dbase, dst_row, lt, fa.inverse != 0);
     if (tn >= a.ntiles) break;
     __syncthreads();
     t = tn;
