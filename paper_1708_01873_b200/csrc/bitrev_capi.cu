@@ -839,6 +839,42 @@ int launch_scatter(const void* local, char* const* peer, int b_local, int g, int
   return BITREV_ETILE;
 }
 
+// Streams and events of bitrev_host_pipeline, created on a thread's first
+// call per device and kept for the thread's lifetime (round 1 created and
+// destroyed 3 streams and 10 events on every call).  Per thread, so calls
+// from several host threads never share them; never destroyed, because a
+// thread_local destructor may run after the CUDA runtime has shut down.
+constexpr int kPipeSlots = 3;
+struct PipeRes {
+  bool ok = false;
+  cudaStream_t sin = nullptr, sk = nullptr, sout = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[kPipeSlots] = {}, ev_k[kPipeSlots] = {},
+              ev_out[kPipeSlots] = {};
+};
+
+cudaError_t pipe_resources(PipeRes** out) {
+  thread_local PipeRes res[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  PipeRes& r = res[dev];
+  if (!r.ok) {
+    if ((e = cudaStreamCreateWithFlags(&r.sin, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&r.sk, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&r.sout, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&r.ev_start, cudaEventDisableTiming)) != cudaSuccess) return e;
+    for (int i = 0; i < kPipeSlots; ++i) {
+      if ((e = cudaEventCreateWithFlags(&r.ev_in[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&r.ev_k[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&r.ev_out[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    r.ok = true;
+  }
+  *out = &r;
+  return cudaSuccess;
+}
+
 cudaStream_t st_of(void* stream) { return static_cast<cudaStream_t>(stream); }
 
 template <int E, int QX, int QZ>
@@ -1086,32 +1122,27 @@ int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int
   if (!host_src || !host_dst) return BITREV_ENULL;
   for (int64_t k = 0; k < count; ++k)
     if (!host_src[k] || !host_dst[k]) return BITREV_ENULL;
-  constexpr int kSlots = 3;
+  constexpr int kSlots = kPipeSlots;
   const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
   const int64_t n = int64_t(1) << b;
   cudaStream_t user = static_cast<cudaStream_t>(stream);
-  cudaStream_t sin = nullptr, sk = nullptr, sout = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_in[kSlots] = {}, ev_k[kSlots] = {}, ev_out[kSlots] = {};
   void* own = nullptr;
   char* slots = static_cast<char*>(dev_scratch);
   cudaError_t e = cudaSuccess;
+  PipeRes* pr = nullptr;
+  cudaStream_t sin = nullptr, sk = nullptr, sout = nullptr;
 #define PIPE_TRY(x)              \
   do {                           \
     e = (x);                     \
     if (e != cudaSuccess) goto done; \
   } while (0)
-  PIPE_TRY(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
-  PIPE_TRY(cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking));
-  PIPE_TRY(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
-  PIPE_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-  for (int i = 0; i < kSlots; ++i) {
-    PIPE_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
-    PIPE_TRY(cudaEventCreateWithFlags(&ev_k[i], cudaEventDisableTiming));
-    PIPE_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
-  }
+  PIPE_TRY(pipe_resources(&pr));
+  sin = pr->sin;
+  sk = pr->sk;
+  sout = pr->sout;
   // order after the caller's prior work
-  PIPE_TRY(cudaEventRecord(ev_start, user));
-  PIPE_TRY(cudaStreamWaitEvent(sin, ev_start, 0));
+  PIPE_TRY(cudaEventRecord(pr->ev_start, user));
+  PIPE_TRY(cudaStreamWaitEvent(sin, pr->ev_start, 0));
   if (!slots) {
     PIPE_TRY(cudaMallocAsync(&own, kSlots * bytes, sin));
     slots = static_cast<char*>(own);
@@ -1119,22 +1150,22 @@ int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int
   for (int64_t k = 0; k < count; ++k) {
     const int s = (int)(k % kSlots);
     char* buf = slots + (size_t)s * bytes;
-    if (k >= kSlots) PIPE_TRY(cudaStreamWaitEvent(sin, ev_out[s], 0));  // slot drained
+    if (k >= kSlots) PIPE_TRY(cudaStreamWaitEvent(sin, pr->ev_out[s], 0));  // slot drained
     // the host source may be the destination of a step still in flight
     for (int64_t j = k - 1; j >= 0 && j > k - kSlots; --j) {
       const uintptr_t a0 = (uintptr_t)host_src[k], d0 = (uintptr_t)host_dst[j];
       if (a0 < d0 + bytes && d0 < a0 + bytes)
-        PIPE_TRY(cudaStreamWaitEvent(sin, ev_out[j % kSlots], 0));
+        PIPE_TRY(cudaStreamWaitEvent(sin, pr->ev_out[j % kSlots], 0));
     }
     PIPE_TRY(cudaMemcpyAsync(buf, host_src[k], bytes, cudaMemcpyHostToDevice, sin));
-    PIPE_TRY(cudaEventRecord(ev_in[s], sin));
-    PIPE_TRY(cudaStreamWaitEvent(sk, ev_in[s], 0));
+    PIPE_TRY(cudaEventRecord(pr->ev_in[s], sin));
+    PIPE_TRY(cudaStreamWaitEvent(sk, pr->ev_in[s], 0));
     rc = bitrev_inplace(buf, b, elem_bytes, batch, n, sk);
     if (rc != BITREV_OK) goto done;
-    PIPE_TRY(cudaEventRecord(ev_k[s], sk));
-    PIPE_TRY(cudaStreamWaitEvent(sout, ev_k[s], 0));
+    PIPE_TRY(cudaEventRecord(pr->ev_k[s], sk));
+    PIPE_TRY(cudaStreamWaitEvent(sout, pr->ev_k[s], 0));
     PIPE_TRY(cudaMemcpyAsync(host_dst[k], buf, bytes, cudaMemcpyDeviceToHost, sout));
-    PIPE_TRY(cudaEventRecord(ev_out[s], sout));
+    PIPE_TRY(cudaEventRecord(pr->ev_out[s], sout));
   }
   if (own) {
     // every use of the slots is ordered before the last D2H on sout (each
@@ -1145,20 +1176,11 @@ int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int
   PIPE_TRY(cudaStreamSynchronize(sout));
 done:
 #undef PIPE_TRY
-  // error or not, nothing may still be using the slots or the events below
+  // error or not, nothing may still be using the slots when this returns
   if (sin) cudaStreamSynchronize(sin);
   if (sk) cudaStreamSynchronize(sk);
   if (sout) cudaStreamSynchronize(sout);
   if (own) cudaFree(own);  // only on an error path: the normal path frees stream-ordered
-  for (int i = 0; i < kSlots; ++i) {
-    if (ev_in[i]) cudaEventDestroy(ev_in[i]);
-    if (ev_k[i]) cudaEventDestroy(ev_k[i]);
-    if (ev_out[i]) cudaEventDestroy(ev_out[i]);
-  }
-  if (ev_start) cudaEventDestroy(ev_start);
-  if (sin) cudaStreamDestroy(sin);
-  if (sk) cudaStreamDestroy(sk);
-  if (sout) cudaStreamDestroy(sout);
   if (rc != BITREV_OK) return rc;
   return e == cudaSuccess ? BITREV_OK : (int)e;
 }
@@ -1174,6 +1196,24 @@ int bitrev_transpose_square(void* a, int h, int elem_bytes, int64_t batch, int64
   if (batch == 1) batch_stride = n;
   if (h == 0) return BITREV_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool vec_ok = aligned16(a) && ((batch_stride * elem_bytes) % 16 == 0);
+  // vectorised tile pairs: 256-byte rows (512 for complex128)
+  const int tq = elem_bytes == 4 ? 6 : 5;
+  if (vec_ok && (elem_bytes == 4 || elem_bytes == 8 || elem_bytes == 16) && h >= tq) {
+    const uint64_t nt = 1ull << (h - tq);
+    const uint64_t work = nt * (nt + 1) / 2 * (uint64_t)batch;
+#define TRT_CASE(E_, Q_)                                                                   \
+  if (elem_bytes == E_) {                                                                  \
+    using T = TrTile<E_, Q_>;                                                              \
+    auto kern = transpose_tile_kernel<E_, Q_>;                                             \
+    const int per_sm = prepare_kernel(kern, T::THREADS, 2 * T::BYTES);                    \
+    kern<<<grid_for(work, per_sm), T::THREADS, 2 * T::BYTES, st>>>(static_cast<char*>(a), h, \
+                                                                   batch, batch_stride * E_); \
+    return finish_launch();                                                                \
+  }
+    TRT_CASE(4, 6) TRT_CASE(8, 5) TRT_CASE(16, 5)
+#undef TRT_CASE
+  }
   const int side = 1 << h;
   const int ts = side < kTT ? side : kTT;
   const uint64_t nt = (uint64_t)(side / ts);

@@ -2170,6 +2170,99 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Vectorised square in-place transpose: tile pairs {(I, J), (J, I)}, I <= J,
+// of 2^Q x 2^Q tiles (256-512-byte rows), both tiles loaded with 16-byte
+// vectors before either is written (the pair's regions belong to it alone).
+// The tile path of the bit-reversal kernels with the reversals taken out:
+// each thread loads V consecutive rows at one 16-byte column, a V x V
+// register transpose makes V destination vectors, XOR-swizzled STS, barrier,
+// then LDS.128 -> STG.128 along the transposed rows.
+template <int E, int Q>
+struct TrTile {
+  static constexpr int S = 1 << Q, V = 16 / E, LV = const_log2(V);
+  static constexpr int CH = S / V;          // 16-byte chunks per row
+  static constexpr int ITEMS = CH * CH;      // load items (V rows each)
+  static constexpr int THREADS = 256;
+  static constexpr int IPT = ITEMS / THREADS;
+  static constexpr int WPT = S * CH / THREADS;
+  static constexpr int BYTES = S * S * E;
+  static_assert(CH >= 8 && ITEMS % THREADS == 0, "tile geometry");
+};
+
+template <int E, int J>
+__device__ __forceinline__ uint4 xpose_nat(const uint4 (&a)[16 / E]) {
+  if constexpr (E == 4) return make_uint4(comp<J>(a[0]), comp<J>(a[1]), comp<J>(a[2]), comp<J>(a[3]));
+  else return xpose<E, J>(a);  // E = 8 / 16: already in natural row order
+}
+
+template <int E, int Q>
+__global__ void __launch_bounds__(TrTile<E, Q>::THREADS)
+    transpose_tile_kernel(char* a, int h, int64_t batch, int64_t bstride) {
+  using T = TrTile<E, Q>;
+  extern __shared__ __align__(16) uint4 smem[];
+  uint4* U0 = smem;
+  uint4* U1 = smem + T::S * T::CH;
+  const uint64_t nt = 1ull << (h - Q);             // tiles per side
+  const uint64_t npairs = nt * (nt + 1) / 2;
+  const uint64_t row_stride = (uint64_t)E << h;     // bytes per matrix row
+  const uint64_t total = npairs * (uint64_t)batch;
+  auto swz = [&](int z, int col) { return z * T::CH + (col ^ ((z >> T::LV) & 7)); };
+  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    const uint64_t bi = w / npairs, p = w - bi * npairs;
+    // p -> (I, J), I <= J: J = largest with J (J + 1) / 2 <= p
+    uint64_t J = (uint64_t)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+    while (J * (J + 1) / 2 > p) --J;
+    while ((J + 1) * (J + 2) / 2 <= p) ++J;
+    const uint64_t I = p - J * (J + 1) / 2;
+    char* m = a + bi * (uint64_t)bstride;
+    char* tA = m + (I << Q) * row_stride + ((J << Q) * E);  // tile (I, J)
+    char* tB = m + (J << Q) * row_stride + ((I << Q) * E);  // tile (J, I)
+    const bool diag = I == J;
+    uint4 r0[T::IPT][T::V], r1[T::IPT][T::V];
+#pragma unroll
+    for (int it = 0; it < T::IPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int c = id % T::CH, g = id / T::CH;
+#pragma unroll
+      for (int k = 0; k < T::V; ++k) {
+        const uint64_t off = (uint64_t)(g * T::V + k) * row_stride + (uint64_t)c * 16;
+        r0[it][k] = ld_plain(tA + off);
+        if (!diag) r1[it][k] = ld_plain(tB + off);
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < T::IPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int c = id % T::CH, g = id / T::CH;
+      // source rows g*V + k, column chunk c -> destination rows c*V + j, chunk g
+      U0[swz(c * T::V, g)] = xpose_nat<E, 0>(r0[it]);
+      if (!diag) U1[swz(c * T::V, g)] = xpose_nat<E, 0>(r1[it]);
+      if constexpr (T::V > 1) {
+        U0[swz(c * T::V + 1, g)] = xpose_nat<E, 1>(r0[it]);
+        if (!diag) U1[swz(c * T::V + 1, g)] = xpose_nat<E, 1>(r1[it]);
+      }
+      if constexpr (T::V > 2) {
+        U0[swz(c * T::V + 2, g)] = xpose_nat<E, 2>(r0[it]);
+        U0[swz(c * T::V + 3, g)] = xpose_nat<E, 3>(r0[it]);
+        if (!diag) {
+          U1[swz(c * T::V + 2, g)] = xpose_nat<E, 2>(r1[it]);
+          U1[swz(c * T::V + 3, g)] = xpose_nat<E, 3>(r1[it]);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < T::WPT; ++it) {
+      const int id = it * T::THREADS + threadIdx.x;
+      const int col = id % T::CH, z = id / T::CH;
+      const uint64_t off = (uint64_t)z * row_stride + (uint64_t)col * 16;
+      st_vec(tB + off, U0[swz(z, col)]);         // tile (I, J) transposed -> (J, I)
+      if (!diag) st_vec(tA + off, U1[swz(z, col)]);
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // even-odd split (replaces _even_odd, src/recursive.py:84-93), out of place.
 

@@ -149,19 +149,25 @@ def transpose_square_inplace(region, h: int) -> None:
 def even_odd_permute(array, b: int, scratch=None) -> None:
     """Evens to the bottom half, odds to the top (src/recursive.py:96-107).
 
-    The reference parks the odds in an n/2 scratch; the GPU kernel writes the
-    split out of place into a device buffer which is then copied back.
+    The reference parks the odds in an n/2 scratch.  On the device the split
+    is the index rotation i -> (i >> 1) | ((i & 1) << (b - 1)), which factors
+    into two bit reversals: the full width, then each half (rev_{b-1} on the
+    low b-1 bits after rev_b puts bit 0 on top).  Both run in place on the
+    tile kernels, so no scratch is touched (it is validated like the
+    reference's) and no n-element temporary is allocated.
     """
     check_width(b)
     a = as_tensor(array)
     if a.dim() != 1 or a.shape[0] != (1 << b):
         raise ValueError(f"array length {a.shape[0]} does not match 2**{b}")
     _ensure_scratch(scratch, a.shape[0] >> 1, a.dtype)
+    if b == 1:
+        return  # [a0, a1] is already split
+    _core.elem_bytes(a)
+    on_device = a.is_cuda and a.is_contiguous()
     dev = a.device if a.is_cuda else _core.require_cuda()
-    src = a if (a.is_cuda and a.is_contiguous()) else a.to(dev).contiguous()
-    out = torch.empty(src.shape, dtype=src.dtype, device=dev)
-    n = 1 << b
-    with torch.cuda.device(dev):
-        _lib.call("bitrev_even_odd", src.data_ptr(), out.data_ptr(), b, _core.elem_bytes(src), 1,
-                  n, n, _core._stream_ptr(dev))
-    a.copy_(out)
+    work = a if on_device else a.to(dev, copy=True).contiguous()  # host / strided: staged once
+    _core.launch_inplace(work, b)
+    _core.launch_inplace(work.view(2, -1), b - 1)
+    if work is not a:
+        a.copy_(work)
