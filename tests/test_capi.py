@@ -53,6 +53,22 @@ def test_error_codes_without_gpu():
     assert lib.bitrev_transpose_square(p, -1, 8, 1, 0, None) == -1
     assert lib.bitrev_sharded_unpack(p, p, 4, 5, 8, None) == -6
     assert lib.bitrev_apply_pairs(p, p, 0, 8, None) == 0  # empty list is a no-op
+    assert lib.bitrev_apply_pairs_ordered(p, p, 0, 8, None) == 0
+    assert lib.bitrev_apply_pairs_ordered(p, p, -1, 8, None) == -4
+    assert lib.bitrev_apply_pairs_ordered(p, None, 3, 8, None) == -3
+    assert lib.bitrev_swap_schedule(0, p, None) == -1  # width
+    assert lib.bitrev_swap_schedule(49, p, None) == -1
+    assert lib.bitrev_swap_schedule(5, None, None) == -3
+    assert lib.bitrev_swap_schedule(1, p, None) == 0  # no pairs at width 1
+    # sharded pack: width, element size, plan shape (2g + chunk bits <= b_local), overlap
+    assert lib.bitrev_sharded_pack(p, p + 2048, 0, 1, 0, 8, None) == -1
+    assert lib.bitrev_sharded_pack(p, p + 2048, 10, 1, 0, 2, None) == -2
+    assert lib.bitrev_sharded_pack(p, p + 2048, 10, 4, 0, 8, None) == -6  # G = 16 > 8
+    assert lib.bitrev_sharded_pack(p, p + 2048, 6, 3, 1, 8, None) == -6
+    assert lib.bitrev_sharded_pack(None, p, 10, 1, 0, 8, None) == -3
+    assert lib.bitrev_sharded_pack(p, p + 64, 8, 1, 0, 8, None) == -5
+    assert lib.bitrev_sharded_scatter(p, None, 10, 1, 0, 8, None) == -3
+    assert lib.bitrev_sharded_scatter(p, p, 10, 1, 2, 8, None) == -6  # rank >= G
     for code in (0, -1, -2, -3, -4, -5, -6, -7):
         assert lib.bitrev_strerror(code)
     assert b"overlap" in lib.bitrev_strerror(-5)

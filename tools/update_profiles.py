@@ -1,6 +1,10 @@
-"""Refresh profiles/ from a tools/gpu_round.sh run in gpurun_out/:
-raw ncu pages per workload, traffic.json (what bench.py reports as
-roofline.traffic), the launch list and the bench lines."""
+"""Refresh profiles/ from a tools/gpu_round.sh run in gpurun_out/: raw ncu
+pages per workload, traffic.json (what bench.py reports as roofline.traffic;
+entries of workloads not captured this time are kept), the launch list and
+the bench lines.
+
+    python tools/update_profiles.py r02
+"""
 import csv
 import io
 import json
@@ -11,11 +15,13 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 OUT, PROF = ROOT / "gpurun_out", ROOT / "profiles"
-tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 TIME = {"ns": 1e-3, "us": 1, "ms": 1e3}
 
-traffic = {}
+traffic = json.loads((PROF / "traffic.json").read_text()) if (PROF / "traffic.json").exists() else {}
+
+
 def raw_pages():
     """(workload, raw-page CSV text): exported on the box (prof_<w>_raw.csv),
     else read from a full report (prof_<w>.ncu-rep)."""
@@ -33,7 +39,7 @@ def raw_pages():
 
 for w, raw in raw_pages():
     rows = list(csv.reader(io.StringIO(raw)))
-    if len(rows) < 3:
+    if len(rows) < 3 or w.startswith("cfg5") or w in ("cfg316",):
         continue
     (PROF / f"{tag}_{w}_kernel_raw.csv").write_text(raw)
     d, u = dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
@@ -52,11 +58,15 @@ traffic["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch fro
                     "of the bench's own kernel. Writes still in L2 when a kernel ends are not "
                     "counted (all of cfg1's 16 MiB output stays in L2).")
 (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
-shutil.copy(OUT / "launches_cfg2.csv", PROF / f"{tag}_cfg2_launches.csv")
+if (OUT / "launches_default.csv").exists():
+    shutil.copy(OUT / "launches_default.csv", PROF / f"{tag}_default_launches.csv")
 with open(PROF / f"{tag}_bench_lines.jsonl", "w") as fh:
-    for f in ("bench_cfg2.json", "bench_all.jsonl", "bench_ref.json"):
-        fh.write((OUT / f).read_text())
-for w, v in traffic.items():
+    for f in ("bench_default.json", "bench_all.jsonl", "bench_ref.json"):
+        if (OUT / f).exists():
+            for line in (OUT / f).read_text().splitlines():
+                if line.startswith("{"):
+                    fh.write(line + "\n")
+for w, v in sorted(traffic.items()):
     if not w.startswith("_"):
-        print(f"{w:10s} {v['dram_bytes_per_launch'] / 1e9:8.3f} GB {v['duration_us_cold']:9.1f} us "
+        print(f"{w:12s} {v['dram_bytes_per_launch'] / 1e9:8.3f} GB {v['duration_us_cold']:9.1f} us "
               f"dram {v['dram_active_pct']}% regs {v['registers']} grid {v['grid']} {v['kernel'][:48]}")
