@@ -931,7 +931,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks,
         "step_ms": {"median": statistics.median(step_s) * 1e3, "min": min(step_s) * 1e3,
-                    "max": max(step_s) * 1e3},
+                    "max": max(step_s) * 1e3, "all": [round(t * 1e3, 4) for t in step_s]},
     }
     if sweep is not None:
         line["width_sweep"] = sweep

@@ -224,6 +224,11 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
   auto kern = bitrev_oop_tile_kernel<E, Q, NT, false>;
   if constexpr (E == 16 && Q == 6 && NT == BITREV_TILE_THREADS)
     if (stream_stores(E, b, batch)) kern = bitrev_oop_tile_kernel<E, Q, NT, true>;
+  if constexpr (E == 16 && Q == 5 && NT == BITREV_TILE_THREADS) {
+    static const int minb = env_int("BITREV_B200_SMALL_MINB", 1);  // A/B runs
+    if (minb == 4) kern = bitrev_oop_tile_kernel<E, Q, NT, false, 4>;
+    if (minb == 3) kern = bitrev_oop_tile_kernel<E, Q, NT, false, 3>;
+  }
   const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
   TileArgs a;
   a.src = static_cast<const char*>(src);

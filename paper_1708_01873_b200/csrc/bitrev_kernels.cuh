@@ -368,8 +368,8 @@ __device__ __forceinline__ uint64_t pair_from_index(uint64_t w, int m) {
 // ---------------------------------------------------------------------------
 // out-of-place tile kernel (replaces _cobra_copy, src/permutations.py:225-249)
 
-template <int E, int Q, int NT = BITREV_TILE_THREADS, bool CS = false>
-__global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, BITREV_MINB_OOP)
+template <int E, int Q, int NT = BITREV_TILE_THREADS, bool CS = false, int MINB = BITREV_MINB_OOP>
+__global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, MINB)
     bitrev_oop_tile_kernel(TileArgs a) {
   using T = Tile<E, Q, NT>;
   extern __shared__ __align__(16) uint4 smem[];
