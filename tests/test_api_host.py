@@ -209,7 +209,7 @@ def test_bench_config_defaults_match_reference_fields():
     ({"element_kind": "c64"}, "element kind"),
     ({"cobra_q": -1}, "cobra_q"),
     ({"memory_cap_bytes": 0}, "memory_cap_bytes"),
-    ({"base_bits": 0}, ""),
+    ({"base_bits": 0}, "base_bits"),
 ])
 def test_bench_config_validation(kw, frag):
     with pytest.raises(ValueError, match=frag):
