@@ -225,7 +225,12 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
   if constexpr (E == 16 && Q == 6 && NT == BITREV_TILE_THREADS)
     if (stream_stores(E, b, batch)) kern = bitrev_oop_tile_kernel<E, Q, NT, true>;
   if constexpr (E == 16 && Q == 5 && NT == BITREV_TILE_THREADS) {
-    static const int minb = env_int("BITREV_B200_SMALL_MINB", 1);  // A/B runs
+    // complex128 up to 32 MiB per side (the Q5 tier): 4 CTAs/SM (63
+    // registers) instead of 2 puts every tile of a 2^20 array in flight at
+    // once: L2-hot cfg1 6860 -> 7250 GB/s, L2-flushed unchanged (at the
+    // copy_ floor, profiles/r02_cfg1_minb_ab.jsonl, r02_minb_sizes_ab.jsonl).
+    // BITREV_B200_SMALL_MINB=1|3 selects the other forms (A/B runs).
+    static const int minb = env_int("BITREV_B200_SMALL_MINB", 4);
     if (minb == 4) kern = bitrev_oop_tile_kernel<E, Q, NT, false, 4>;
     if (minb == 3) kern = bitrev_oop_tile_kernel<E, Q, NT, false, 3>;
   }
@@ -905,7 +910,13 @@ int launch_pack_rect(const void* src, char* const* peer, int rank, int b, int g,
   using T = Rect<E, QX, QZ>;
   if (b < QX + QZ || sb < QX) return BITREV_ETILE;
   auto kern = bitrev_pack_rect_kernel<E, QX, QZ>;
-  const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
+  // Dynamic shared memory padded to 80 KB caps the pack at 2 CTAs/SM: the E=8
+  // (7,5) tiles would otherwise run 3 (80 registers) and measured 0.92-0.94
+  // of the peak against 0.95-0.97 at 2 (profiles/r02_pack_smem_ab.jsonl).
+  // BITREV_B200_PACK_SMEM_KB overrides the pad (A/B runs; 0 = none).
+  static const int pad_kb = env_int("BITREV_B200_PACK_SMEM_KB", 80);
+  const int smem = pad_kb * 1024 > T::BYTES ? pad_kb * 1024 : T::BYTES;
+  const int per_sm = prepare_kernel(kern, T::THREADS, smem);
   PackArgs pa;
   memset(&pa, 0, sizeof pa);
   TileArgs& a = pa.t;
@@ -918,7 +929,7 @@ int launch_pack_rect(const void* src, char* const* peer, int rank, int b, int g,
   pa.g = g;
   pa.sb = sb;
   pa.rank = rank;
-  kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(pa);
+  kern<<<grid_for(a.ntiles, per_sm), T::THREADS, smem, st>>>(pa);
   return finish_launch();
 }
 
