@@ -512,7 +512,9 @@ int launch_oop_rect(const void* src, void* dst, int b, int64_t batch, int64_t sb
   auto kern = bitrev_oop_rect_kernel<E, QX, QZ, false>;
   if constexpr ((E == 4 && QX == 8 && QZ == 6) || (E == 8 && QX == 7 && QZ == 5))
     if (stream_stores(E, b, batch)) kern = bitrev_oop_rect_kernel<E, QX, QZ, true>;
-  const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);
+  static const int pad_kb = env_int("BITREV_B200_RECT_SMEM_KB", 0);  // A/B runs: cap CTAs/SM
+  const int smem = pad_kb * 1024 > T::BYTES ? pad_kb * 1024 : T::BYTES;
+  const int per_sm = prepare_kernel(kern, T::THREADS, smem);
   TileArgs a;
   a.src = static_cast<const char*>(src);
   a.dst = static_cast<char*>(dst);
@@ -525,7 +527,7 @@ int launch_oop_rect(const void* src, void* dst, int b, int64_t batch, int64_t sb
   a.npairs = 0;
   a.batch = batch;
   const int grid = grid_for(a.ntiles, per_sm);
-  kern<<<grid, T::THREADS, T::BYTES, st>>>(a);
+  kern<<<grid, T::THREADS, smem, st>>>(a);
   return finish_launch();
 }
 
