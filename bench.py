@@ -9,7 +9,9 @@ A "step" is one permutation of one batch of synthetic input (BASELINE.json
 configs).  BASELINE.json quotes its metric "vs log2 n" on no single config,
 so the N=1 line is the largest single-GPU config: cfg3-16 = n=2^30 complex128
 out of place (16 GiB per side); the same line carries cfg3-4 / cfg3-8 (the
-element-width sweep of config 3) under "width_sweep".  With N > 1 the default
+element-width sweep of config 3) under "width_sweep", and the other configs
+(cfg1, cfg2, cfg4, cfg4-fft7, cfg5's array on one GPU) under "other_configs",
+each timed with the same protocol in the same run.  With N > 1 the default
 is cfg5, the one config that shards a single array: n=2^32 complex64 split by
 its top log2 N index bits, local reversal + NCCL all_to_all_single over
 NVLink + local interleave, with per-phase times and all-to-all bus bandwidth.
@@ -480,33 +482,57 @@ def time_steps(torch, step, steps, stream, flush=None):
     return [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
 
 
-def width_sweep(torch, dev, peak, steps):
-    """cfg3-4 and cfg3-8 (config 3's element-width sweep) on the same device,
-    same protocol (inputs far larger than the L2, no flush), fewer steps."""
+def plain_step(wl, x, y, stream):
+    """The device step of a single-GPU workload on resident buffers x (, y)."""
     from paper_1708_01873_b200 import _core, _lib
+
+    b, _, E, inplace, _, _ = WORKLOADS[wl]
+    if wl == "cfg4-fft7":
+        rows = x.shape[0]
+        return lambda: _lib.call("bitrev_dit_prepass", x.data_ptr(), y.data_ptr(), b, E, rows,
+                                 1 << b, 1 << b, 7, 0, stream.cuda_stream)
+    if inplace:
+        return lambda: _core.launch_inplace(x, b)
+    return lambda: _core.launch_oop(x, y, b)
+
+
+def config_sweep(torch, dev, peak, steps, workloads):
+    """The other BASELINE configs on the same device in the same run, each
+    with the main line's protocol (L2 flush before every step below 4x the
+    L2, CUDA events per step, W = 3 warm-up steps), fewer steps; cfg5 is its
+    whole 2^32-element array on this one GPU."""
+    from paper_1708_01873_b200 import _lib
 
     out = {}
     stream = torch.cuda.current_stream(dev)
-    for w in ("cfg3-4", "cfg3-8"):
-        b, dtname, E, _, _, desc = WORKLOADS[w]
-        x = torch.empty((1 << b) * E, dtype=torch.uint8, device=dev).random_(0, 256)
-        x = x.view(getattr(torch, dtname))
-        y = torch.empty_like(x)
-
-        def step():
-            _core.launch_oop(x, y, b)
-
-        for _ in range(3):
+    for w in workloads:
+        b, dtname, E, inplace, batch, desc = WORKLOADS[w]
+        shape = (batch, 1 << b) if batch > 1 else (1 << b,)
+        n = batch << b
+        x = torch.empty(n * E, dtype=torch.uint8, device=dev).random_(0, 256)
+        x = x.view(getattr(torch, dtname)).view(shape)
+        y = None if inplace else torch.empty_like(x)
+        step = plain_step(w, x, y, stream)
+        nbytes = 2 * n * E
+        flush = Flush(torch, dev) if nbytes < 4 * L2_BYTES else None
+        for _ in range(5):
+            if flush is not None:
+                flush.zero_()
             step()
         torch.cuda.synchronize()
-        ts = time_steps(torch, step, steps, stream)
-        nbytes = 2 * (1 << b) * E
+        ts = time_steps(torch, step, steps, stream, flush)
         v = nbytes * len(ts) / sum(ts) / 1e9
         q, path = _lib.last_tile()
         out[w] = {"value": v, "unit": "GB/s", "gelem_per_s": v / (2 * E), "frac": v / peak,
-                  "ms_per_step": sum(ts) / len(ts) * 1e3, "steps": steps, "tile_bits": q,
-                  "tile_path": path, "workload": desc}
-        del x, y
+                  "ms_per_step": sum(ts) / len(ts) * 1e3,
+                  "median_ms": statistics.median(ts) * 1e3, "steps": steps,
+                  "step_ms_all": [round(t * 1e3, 4) for t in ts],
+                  "tile_bits": None if w == "cfg4-fft7" else q,
+                  "tile_path": None if w == "cfg4-fft7" else path,
+                  "l2": "flushed before every step" if flush else "inputs larger than L2, no flush",
+                  "workload": desc}
+        del x, y, flush
+        gc.collect()
         torch.cuda.empty_cache()
     return out
 
@@ -755,18 +781,8 @@ def main():
         if not (args.p2p and world > 1):
             def step():
                 return sharded.sharded_bitrev(x, b, chunks=chunks)
-    elif args.workload == "cfg4-fft7":
-        n_rows = shape[0]
-
-        def step():
-            _lib.call("bitrev_dit_prepass", x.data_ptr(), y.data_ptr(), b, E, n_rows, 1 << b,
-                      1 << b, 7, 0, stream.cuda_stream)
-    elif inplace:
-        def step():
-            _core.launch_inplace(x, b)
     else:
-        def step():
-            _core.launch_oop(x, y, b)
+        step = plain_step(args.workload, x, y, stream)
 
     need_flush = 2 * bytes_local < 4 * L2_BYTES and args.workload != "cfg5"
     flush = Flush(torch, dev) if need_flush else None
@@ -875,13 +891,15 @@ def main():
         elif rank == 0:
             e2e, e2e_single = e2e_host(torch, br, x, b, E, inplace, args.workload, args.steps,
                                        stream)
-    sweep = None
-    if args.workload == "cfg3-16" and not args.no_sweep:
+    sweep = others = None
+    if args.workload == "cfg3-16" and not args.no_sweep and world == 1:
         del x, y
         x = y = None
         gc.collect()
         torch.cuda.empty_cache()
-        sweep = width_sweep(torch, dev, peak, max(5, min(args.steps, 10)))
+        sweep = config_sweep(torch, dev, peak, max(5, min(args.steps, 10)), ("cfg3-4", "cfg3-8"))
+        others = config_sweep(torch, dev, peak, max(10, args.steps),
+                              ("cfg1", "cfg2", "cfg4", "cfg4-fft7", "cfg5"))
     sampler.stop()
     clocks = sampler.summary(t_wall0, t_wall1)
 
@@ -935,6 +953,8 @@ def main():
     }
     if sweep is not None:
         line["width_sweep"] = sweep
+    if others is not None:
+        line["other_configs"] = others
     if args.workload == "cfg5":
         line["config"]["exchange"] = exchange
         line["config"]["chunks"] = args.chunks if world > 1 else 1
