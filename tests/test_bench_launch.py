@@ -1,0 +1,65 @@
+"""bench.py's multi-rank launch plumbing.
+
+* CPU: the reference arm under torchrun with two ranks -- rank 0 times the
+  reference's CPU path and prints exactly one JSON line, rank 1 exits 0
+  without work (the driver launches both arms the same way).
+* GPU (one device): cfg4 under torchrun with two ranks on the same GPU over
+  gloo.  cfg4 shards batch rows with no data-path collective, so the ranks'
+  kernels never wait on one another; this checks the barrier / max-over-ranks
+  / one-line plumbing, not multi-GPU performance.
+"""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _torchrun(args, timeout):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"),
+           *args]
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1")
+    return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+
+
+def _json_lines(out):
+    return [json.loads(x) for x in out.splitlines() if x.startswith("{")]
+
+
+def test_reference_arm_two_ranks():
+    p = _torchrun(["--impl", "reference", "--gpus", "2", "--workload", "cfg1", "--steps", "2",
+                   "--warmup", "1"], timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = lines[0]
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] in ("port", "reference")
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_cfg4_two_ranks_one_device(cuda):
+    p = _torchrun(["--gpus", "2", "--workload", "cfg4", "--steps", "3", "--warmup", "3",
+                   "--same-device", "--dist-backend", "gloo", "--no-e2e", "--no-soak"],
+                  timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] == 3
+    assert d["config"]["parallelism"] == "batch rows sharded over 2 GPUs"
+    assert d["config"]["per_gpu_bytes_moved"] == 2 * 2048 * (1 << 16) * 8
