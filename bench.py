@@ -111,9 +111,16 @@ def parse():
                     help="skip the 0.5 s clock soak (for profiler runs)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0,
                     help="target seconds of CPU work for the cpu_baseline sample")
+    ap.add_argument("--bits", type=int, default=0,
+                    help="override the workload's log2 n (functional tests of the launch "
+                         "plumbing at small sizes; never for reported numbers)")
     args = ap.parse_args()
     if args.workload is None:
         args.workload = default_workload(dist_env()[0])
+    if args.bits:
+        b, dt, E, ip, batch, desc = WORKLOADS[args.workload]
+        WORKLOADS[args.workload] = (args.bits, dt, E, ip, batch,
+                                    f"{desc} [TEST SIZE: n=2^{args.bits}]")
     return args
 
 

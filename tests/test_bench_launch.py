@@ -63,3 +63,25 @@ def test_cfg4_two_ranks_one_device(cuda):
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] == 3
     assert d["config"]["parallelism"] == "batch rows sharded over 2 GPUs"
     assert d["config"]["per_gpu_bytes_moved"] == 2 * 2048 * (1 << 16) * 8
+
+
+@pytest.mark.gpu
+def test_cfg5_two_ranks_one_device_gloo(cuda):
+    """cfg5's N > 1 bench path (pack, all_to_all_single rounds, unpack, the
+    per-phase instrumented round, the host-buffer e2e, max over ranks) at a
+    test size, two ranks on one device over gloo: a functional check of the
+    line the SCALE runs print, not a timing."""
+    p = _torchrun(["--gpus", "2", "--workload", "cfg5", "--bits", "24", "--steps", "3",
+                   "--warmup", "3", "--same-device", "--dist-backend", "gloo", "--no-soak"],
+                  timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "strong"
+    assert d["config"]["chunks"] == 4 and "all_to_all_single" in d["config"]["exchange"]
+    assert set(d["phases"]["ms"]) == {"pack", "a2a", "unpack"}
+    assert d["nvlink_roofline"]["busbw_gbs"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == (1 << 23) * 8
+    assert d["gpu_launches"] == 3 * (1 + 4)  # per step: one pack, one unpack per round
+    assert "TEST SIZE" in d["config"]["workload"]
