@@ -105,6 +105,11 @@ def sharded_bitrev(local: torch.Tensor, b: int, group=None, *, chunks: int = 1,
     C = 1 << (b_local - g)
     if chunks < 1 or chunks & (chunks - 1) or chunks > C:
         raise ValueError(f"chunks must be a power of two in 1..{C}, got {chunks}")
+    if chunks > 1 and (C // chunks < 64 or b_local < 12):
+        # rounds are a pipelining knob only (the output does not depend on
+        # them); sub-chunks shorter than a tile row cannot be packed, and
+        # shards this small gain nothing from overlap
+        chunks = 1
     kb = chunks.bit_length() - 1
     pack = pack or _pack
     unpack = unpack or _unpack

@@ -103,12 +103,13 @@ def _worker(rank, world, port, b, q, chunks=1):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,chunks", [(2, 1), (4, 1), (2, 4), (4, 2), (4, 4)])
-def test_sharded_bitrev_gloo(world, chunks):
+@pytest.mark.parametrize("world,chunks,b", [(2, 1, 10), (4, 1, 10), (2, 4, 14), (4, 2, 14),
+                                            (4, 4, 16), (2, 4, 8)])
+def test_sharded_bitrev_gloo(world, chunks, b):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, 10, q, chunks))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, b, q, chunks))
              for r in range(world)]
     for p in procs:
         p.start()
