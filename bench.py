@@ -106,7 +106,10 @@ def parse():
     ap.add_argument("--chunks", type=int, default=4,
                     help="cfg5: all-to-all rounds (round c+1 on the wire while c is interleaved)")
     ap.add_argument("--p2p", action="store_true",
-                    help="cfg5: fused scatter into peer-mapped symmetric memory instead of NCCL")
+                    help="cfg5: time the fused scatter into peer-mapped symmetric memory as the "
+                         "main line instead of NCCL")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="cfg5, N > 1: skip the fused peer-store companion measurement")
     ap.add_argument("--no-soak", action="store_true",
                     help="skip the 0.5 s clock soak (for profiler runs)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0,
@@ -719,6 +722,48 @@ def cfg5_phases(torch, dist, sharded, x, b, world, reps=3):
     return out
 
 
+def fused_p2p_companion(torch, dist, sharded, x, b, rank, world, steps, stream):
+    """cfg5 at N > 1: the fused local-reversal + peer-store exchange
+    (sharded_bitrev_p2p over torch symmetric memory) beside the NCCL line.
+    Every rank must set up its peer views (agreed by an all-reduce), the
+    fused result must equal the NCCL result byte for byte on every rank, and
+    only then is it timed (CUDA events per step, max over ranks).  Any failure
+    is reported in the returned record instead of the value."""
+    ok, why = 1, ""
+    try:
+        peers, barrier, keep = sharded.symmetric_recv(x.numel(), x.dtype, x.device)
+    except Exception as exc:  # no symmetric memory / peer mapping on this node
+        ok, why = 0, f"{type(exc).__name__}: {exc}"[:300]
+    flag = torch.tensor([ok], dtype=torch.int32, device=x.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if not int(flag.item()):
+        return {"value": None, "error": why or "peer views unavailable on another rank"}
+    ref = sharded.sharded_bitrev(x, b, chunks=1)
+    got = sharded.sharded_bitrev_p2p(x, b, peers, rank, barrier)
+    same = torch.tensor([int(torch.equal(ref.view(torch.uint8), got.view(torch.uint8)))],
+                        dtype=torch.int32, device=x.device)
+    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    del ref, got
+    if not int(same.item()):
+        return {"value": None, "error": "fused result differs from the NCCL result"}
+    step = lambda: sharded.sharded_bitrev_p2p(x, b, peers, rank, barrier)  # noqa: E731
+    for _ in range(3):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ts = time_steps(torch, step, steps, stream)
+    t = torch.tensor([sum(ts)], dtype=torch.float64, device=x.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    job = float(t.item())
+    E = x.element_size()
+    del keep
+    return {"value": (1 << b) * 2 * E * steps / job / 1e9, "unit": "GB/s",
+            "ms_per_step": job / steps * 1e3, "steps": steps,
+            "path": "bitrev_sharded_scatter (rectangular tiles stored into the peers' "
+                    "symmetric-memory receive buffers over NVLink), barrier, unpack, barrier",
+            "checked": "byte-equal to the NCCL result on every rank"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -833,9 +878,12 @@ def main():
     sampler.mark("load1")
 
     # cfg5: per-phase times and all-to-all bandwidth (one round, instrumented)
-    phases = None
+    phases = fused = None
     if args.workload == "cfg5" and not args.p2p:
         phases = cfg5_phases(torch, dist, sharded, x, b, world)
+        if world > 1 and args.dist_backend == "nccl" and not args.no_fused:
+            fused = fused_p2p_companion(torch, dist, sharded, x, b, rank, world,
+                                        max(3, min(args.steps, 10)), stream)
 
     # same-harness reference: torch copy_ of the same bytes with the same
     # flush protocol (a device copy moves 2*n*E bytes, like one permutation)
@@ -976,6 +1024,8 @@ def main():
             line["roofline"]["kernel"] = "bitrev oop tile kernel (2^32 elements on one GPU)"
         if phases is not None:
             line["phases"] = phases
+        if fused is not None:
+            line["fused_p2p"] = fused
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args.workload, args.cpu_sample_s)
