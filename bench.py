@@ -612,31 +612,39 @@ def e2e_host(torch, br, x, b, E, inplace, workload, steps, stream):
         e2e = e2e_single
     else:
         # PCIe ceiling for the pipeline, same harness: each step one H2D and one
-        # D2H of the step's bytes on two streams, nothing else (no kernel).
+        # D2H of the step's bytes, both split into 256 MiB pieces over two
+        # streams per direction exactly like the pipeline's copies, no kernel.
         d_in, d_out = torch.empty_like(x), torch.empty_like(x)
         h_out = houts if houts is not None else hosts
-        s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
+        ups = [torch.cuda.Stream(), torch.cuda.Stream()]
+        downs = [torch.cuda.Stream(), torch.cuda.Stream()]
+        chunk = (256 << 20) // x.element_size()
+        fd_in, fd_out = d_in.view(-1), d_out.view(-1)
         for timed in (False, True):
             torch.cuda.synchronize()
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
-            s_up.wait_stream(stream)
-            s_down.wait_stream(stream)
+            for st_ in ups + downs:
+                st_.wait_stream(stream)
             for k in range(reps if timed else 2):
-                with torch.cuda.stream(s_up):
-                    d_in.copy_(hosts[k % nhost], non_blocking=True)
-                with torch.cuda.stream(s_down):
-                    h_out[(k + 1) % nhost].copy_(d_out, non_blocking=True)
-            stream.wait_stream(s_up)
-            stream.wait_stream(s_down)
+                src_h = hosts[k % nhost].view(-1)
+                dst_h = h_out[(k + 1) % nhost].view(-1)
+                for i, o in enumerate(range(0, fd_in.numel(), chunk)):
+                    with torch.cuda.stream(ups[i & 1]):
+                        fd_in[o:o + chunk].copy_(src_h[o:o + chunk], non_blocking=True)
+                    with torch.cuda.stream(downs[i & 1]):
+                        dst_h[o:o + chunk].copy_(fd_out[o:o + chunk], non_blocking=True)
+            for st_ in ups + downs:
+                stream.wait_stream(st_)
             ev1.record(stream)
             torch.cuda.synchronize()
         ceil = bytes_local / (ev0.elapsed_time(ev1) / 1e3 / reps) / 1e9
         e2e["pcie_ceiling_gbs"] = ceil
         e2e["frac_of_pcie_ceiling"] = e2e["value"] / ceil
-        e2e["pcie_ceiling_path"] = ("concurrent pinned H2D + D2H of the step's bytes on two "
-                                    "streams, no kernel (same harness)")
+        e2e["pcie_ceiling_path"] = ("concurrent pinned H2D + D2H of the step's bytes, each "
+                                    "as 256 MiB pieces over two streams per direction, no "
+                                    "kernel (same harness)")
         del d_in, d_out
     del hosts, houts
     gc.collect()

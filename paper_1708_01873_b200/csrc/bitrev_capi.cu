@@ -851,17 +851,23 @@ int launch_scatter(const void* local, char* const* peer, int b_local, int g, int
   return BITREV_ETILE;
 }
 
-// Streams and events of bitrev_host_pipeline, created on a thread's first
-// call per device and kept for the thread's lifetime (round 1 created and
-// destroyed 3 streams and 10 events on every call).  Per thread, so calls
+// Streams and events of the host-buffer entry points, created on a thread's
+// first call per device and kept for the thread's lifetime (round 1 created
+// and destroyed 3 streams and 10 events on every call).  Per thread, so calls
 // from several host threads never share them; never destroyed, because a
 // thread_local destructor may run after the CUDA runtime has shut down.
+//
+// Host <-> device copies are split into 256 MiB chunks alternating over two
+// streams per direction: with 16 GiB pinned buffers the concurrent H2D + D2H
+// of whole arrays reached 88 GB/s, the same bytes in 256 MiB chunks 98-99
+// (tools/pcie_probe2.py -> profiles/r02_pcie_probe2.jsonl).
 constexpr int kPipeSlots = 3;
+constexpr size_t kCopyChunk = size_t(256) << 20;
 struct PipeRes {
   bool ok = false;
-  cudaStream_t sin = nullptr, sk = nullptr, sout = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_in[kPipeSlots] = {}, ev_k[kPipeSlots] = {},
-              ev_out[kPipeSlots] = {};
+  cudaStream_t sin[2] = {}, sk = nullptr, sout[2] = {}, aux = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_b = nullptr;
+  cudaEvent_t ev_in[kPipeSlots][2] = {}, ev_k[kPipeSlots] = {}, ev_out[kPipeSlots][2] = {};
 };
 
 cudaError_t pipe_resources(PipeRes** out) {
@@ -872,19 +878,55 @@ cudaError_t pipe_resources(PipeRes** out) {
   if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   PipeRes& r = res[dev];
   if (!r.ok) {
-    if ((e = cudaStreamCreateWithFlags(&r.sin, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithFlags(&r.sk, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithFlags(&r.sout, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&r.ev_start, cudaEventDisableTiming)) != cudaSuccess) return e;
+    auto stream = [&](cudaStream_t* s) { return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking); };
+    auto event = [&](cudaEvent_t* v) { return cudaEventCreateWithFlags(v, cudaEventDisableTiming); };
+    for (int i = 0; i < 2; ++i) {
+      if ((e = stream(&r.sin[i])) != cudaSuccess) return e;
+      if ((e = stream(&r.sout[i])) != cudaSuccess) return e;
+    }
+    if ((e = stream(&r.sk)) != cudaSuccess) return e;
+    if ((e = stream(&r.aux)) != cudaSuccess) return e;
+    if ((e = event(&r.ev_start)) != cudaSuccess) return e;
+    if ((e = event(&r.ev_a)) != cudaSuccess) return e;
+    if ((e = event(&r.ev_b)) != cudaSuccess) return e;
     for (int i = 0; i < kPipeSlots; ++i) {
-      if ((e = cudaEventCreateWithFlags(&r.ev_in[i], cudaEventDisableTiming)) != cudaSuccess) return e;
-      if ((e = cudaEventCreateWithFlags(&r.ev_k[i], cudaEventDisableTiming)) != cudaSuccess) return e;
-      if ((e = cudaEventCreateWithFlags(&r.ev_out[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = event(&r.ev_k[i])) != cudaSuccess) return e;
+      for (int j = 0; j < 2; ++j) {
+        if ((e = event(&r.ev_in[i][j])) != cudaSuccess) return e;
+        if ((e = event(&r.ev_out[i][j])) != cudaSuccess) return e;
+      }
     }
     r.ok = true;
   }
   *out = &r;
   return cudaSuccess;
+}
+
+// bytes from src to dst as kCopyChunk pieces alternating over s[0] / s[1]
+cudaError_t copy_split(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                       const cudaStream_t (&s)[2]) {
+  for (size_t off = 0, i = 0; off < bytes; off += kCopyChunk, ++i) {
+    const size_t n = bytes - off < kCopyChunk ? bytes - off : kCopyChunk;
+    const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + off,
+                                          static_cast<const char*>(src) + off, n, kind, s[i & 1]);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// A blocking host-buffer call's copy on stream st, split over st and the
+// thread's aux stream; st continues only after both halves.
+cudaError_t copy_split_on(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                          cudaStream_t st) {
+  PipeRes* pr = nullptr;
+  cudaError_t e = pipe_resources(&pr);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaEventRecord(pr->ev_a, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(pr->aux, pr->ev_a, 0)) != cudaSuccess) return e;
+  const cudaStream_t s[2] = {st, pr->aux};
+  if ((e = copy_split(dst, src, bytes, kind, s)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(pr->ev_b, pr->aux)) != cudaSuccess) return e;
+  return cudaStreamWaitEvent(st, pr->ev_b, 0);
 }
 
 cudaStream_t st_of(void* stream) { return static_cast<cudaStream_t>(stream); }
@@ -1085,11 +1127,11 @@ int bitrev_oop_host(const void* host_src, void* host_dst, int b, int elem_bytes,
     dev_dst = static_cast<char*>(own) + bytes;
   }
   const int64_t n = int64_t(1) << b;
-  cudaError_t e = cudaMemcpyAsync(dev_src, host_src, bytes, cudaMemcpyHostToDevice, st);
+  cudaError_t e = copy_split_on(dev_src, host_src, bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     rc = bitrev_oop(dev_src, dev_dst, b, elem_bytes, batch, n, n, stream);
     if (rc == BITREV_OK) {
-      e = cudaMemcpyAsync(host_dst, dev_dst, bytes, cudaMemcpyDeviceToHost, st);
+      e = copy_split_on(host_dst, dev_dst, bytes, cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) rc = (int)e;
     }
   } else {
@@ -1115,11 +1157,11 @@ int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void
     dev_buf = own;
   }
   const int64_t n = int64_t(1) << b;
-  cudaError_t e = cudaMemcpyAsync(dev_buf, host_a, bytes, cudaMemcpyHostToDevice, st);
+  cudaError_t e = copy_split_on(dev_buf, host_a, bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     rc = bitrev_inplace(dev_buf, b, elem_bytes, batch, n, stream);
     if (rc == BITREV_OK) {
-      e = cudaMemcpyAsync(host_a, dev_buf, bytes, cudaMemcpyDeviceToHost, st);
+      e = copy_split_on(host_a, dev_buf, bytes, cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) rc = (int)e;
     }
   } else {
@@ -1148,56 +1190,68 @@ int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int
   char* slots = static_cast<char*>(dev_scratch);
   cudaError_t e = cudaSuccess;
   PipeRes* pr = nullptr;
-  cudaStream_t sin = nullptr, sk = nullptr, sout = nullptr;
 #define PIPE_TRY(x)              \
   do {                           \
     e = (x);                     \
     if (e != cudaSuccess) goto done; \
   } while (0)
   PIPE_TRY(pipe_resources(&pr));
-  sin = pr->sin;
-  sk = pr->sk;
-  sout = pr->sout;
   // order after the caller's prior work
   PIPE_TRY(cudaEventRecord(pr->ev_start, user));
-  PIPE_TRY(cudaStreamWaitEvent(sin, pr->ev_start, 0));
+  for (int i = 0; i < 2; ++i) PIPE_TRY(cudaStreamWaitEvent(pr->sin[i], pr->ev_start, 0));
   if (!slots) {
-    PIPE_TRY(cudaMallocAsync(&own, kSlots * bytes, sin));
+    PIPE_TRY(cudaMallocAsync(&own, kSlots * bytes, pr->sin[0]));
     slots = static_cast<char*>(own);
+    PIPE_TRY(cudaEventRecord(pr->ev_a, pr->sin[0]));  // the allocation, for sin[1]
+    PIPE_TRY(cudaStreamWaitEvent(pr->sin[1], pr->ev_a, 0));
   }
   for (int64_t k = 0; k < count; ++k) {
     const int s = (int)(k % kSlots);
     char* buf = slots + (size_t)s * bytes;
-    if (k >= kSlots) PIPE_TRY(cudaStreamWaitEvent(sin, pr->ev_out[s], 0));  // slot drained
+    auto wait_out = [&](int slot) -> cudaError_t {  // both in-streams after slot's D2H
+      for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) {
+          const cudaError_t r = cudaStreamWaitEvent(pr->sin[i], pr->ev_out[slot][j], 0);
+          if (r != cudaSuccess) return r;
+        }
+      return cudaSuccess;
+    };
+    if (k >= kSlots) PIPE_TRY(wait_out(s));  // slot drained
     // the host source may be the destination of a step still in flight
     for (int64_t j = k - 1; j >= 0 && j > k - kSlots; --j) {
       const uintptr_t a0 = (uintptr_t)host_src[k], d0 = (uintptr_t)host_dst[j];
-      if (a0 < d0 + bytes && d0 < a0 + bytes)
-        PIPE_TRY(cudaStreamWaitEvent(sin, pr->ev_out[j % kSlots], 0));
+      if (a0 < d0 + bytes && d0 < a0 + bytes) PIPE_TRY(wait_out((int)(j % kSlots)));
     }
-    PIPE_TRY(cudaMemcpyAsync(buf, host_src[k], bytes, cudaMemcpyHostToDevice, sin));
-    PIPE_TRY(cudaEventRecord(pr->ev_in[s], sin));
-    PIPE_TRY(cudaStreamWaitEvent(sk, pr->ev_in[s], 0));
-    rc = bitrev_inplace(buf, b, elem_bytes, batch, n, sk);
+    PIPE_TRY(copy_split(buf, host_src[k], bytes, cudaMemcpyHostToDevice, pr->sin));
+    for (int i = 0; i < 2; ++i) {
+      PIPE_TRY(cudaEventRecord(pr->ev_in[s][i], pr->sin[i]));
+      PIPE_TRY(cudaStreamWaitEvent(pr->sk, pr->ev_in[s][i], 0));
+    }
+    rc = bitrev_inplace(buf, b, elem_bytes, batch, n, pr->sk);
     if (rc != BITREV_OK) goto done;
-    PIPE_TRY(cudaEventRecord(pr->ev_k[s], sk));
-    PIPE_TRY(cudaStreamWaitEvent(sout, pr->ev_k[s], 0));
-    PIPE_TRY(cudaMemcpyAsync(host_dst[k], buf, bytes, cudaMemcpyDeviceToHost, sout));
-    PIPE_TRY(cudaEventRecord(pr->ev_out[s], sout));
+    PIPE_TRY(cudaEventRecord(pr->ev_k[s], pr->sk));
+    for (int i = 0; i < 2; ++i) PIPE_TRY(cudaStreamWaitEvent(pr->sout[i], pr->ev_k[s], 0));
+    PIPE_TRY(copy_split(host_dst[k], buf, bytes, cudaMemcpyDeviceToHost, pr->sout));
+    for (int i = 0; i < 2; ++i) PIPE_TRY(cudaEventRecord(pr->ev_out[s][i], pr->sout[i]));
   }
+  // sout[0] after every D2H (each D2H after its kernel, each kernel after its H2D)
+  PIPE_TRY(cudaEventRecord(pr->ev_b, pr->sout[1]));
+  PIPE_TRY(cudaStreamWaitEvent(pr->sout[0], pr->ev_b, 0));
   if (own) {
-    // every use of the slots is ordered before the last D2H on sout (each
-    // kernel waits for its H2D, each D2H for its kernel)
-    PIPE_TRY(cudaFreeAsync(own, sout));
+    PIPE_TRY(cudaFreeAsync(own, pr->sout[0]));
     own = nullptr;
   }
-  PIPE_TRY(cudaStreamSynchronize(sout));
+  PIPE_TRY(cudaStreamSynchronize(pr->sout[0]));
 done:
 #undef PIPE_TRY
   // error or not, nothing may still be using the slots when this returns
-  if (sin) cudaStreamSynchronize(sin);
-  if (sk) cudaStreamSynchronize(sk);
-  if (sout) cudaStreamSynchronize(sout);
+  if (pr) {
+    for (int i = 0; i < 2; ++i) {
+      cudaStreamSynchronize(pr->sin[i]);
+      cudaStreamSynchronize(pr->sout[i]);
+    }
+    cudaStreamSynchronize(pr->sk);
+  }
   if (own) cudaFree(own);  // only on an error path: the normal path frees stream-ordered
   if (rc != BITREV_OK) return rc;
   return e == cudaSuccess ? BITREV_OK : (int)e;
