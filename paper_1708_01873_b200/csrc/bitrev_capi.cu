@@ -166,7 +166,9 @@ int set_pair_work(TileArgs& a, int64_t batch, bool compact, int per_sm) {
   }
   a.npairs = pair_count(a.m);
   a.ntiles = (uint64_t)batch * a.npairs;
-  const int grid = grid_for(a.ntiles, per_sm);  // every item is real work: no parity trick
+  // BITREV_B200_IP_GRID_MULT: launch that many times the resident CTAs (A/B runs)
+  static const int mult = env_int("BITREV_B200_IP_GRID_MULT", 1);
+  const int grid = grid_for(a.ntiles, per_sm * (mult > 0 ? mult : 1));  // every item is real work
   a.step_b = (uint64_t)grid / a.npairs;
   a.step_w = (uint64_t)grid % a.npairs;
   return grid;

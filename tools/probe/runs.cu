@@ -183,6 +183,76 @@ void run_bulk(char* s, char* d, uint64_t bytes, int sms, int cps) {
          (unsigned long long)used, R, NS, cps, 2.0 * used / t0 / 1e6, 2.0 * used / t1 / 1e6);
 }
 
+struct u8v { unsigned v[8]; };
+__device__ __forceinline__ u8v ldg256(const void* p) {
+  u8v r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                 "=r"(r.v[6]), "=r"(r.v[7]) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ u8v ldp256(const void* p) {
+  u8v r;
+  asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                 "=r"(r.v[6]), "=r"(r.v[7]) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg256(void* p, const u8v& a) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.v[0]), "r"(a.v[1]),
+               "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]) : "memory");
+}
+// grid-stride copy with 32-byte vectors (LDG.256 / STG.256)
+__global__ void __launch_bounds__(256) copy_lin256(const char* s, char* d, uint64_t n32) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n32; i += 4 * stride) {
+    u8v a = ldg256(s + 32 * i), b = ldg256(s + 32 * (i + stride)), c = ldg256(s + 32 * (i + 2 * stride)),
+        e = ldg256(s + 32 * (i + 3 * stride));
+    stg256(d + 32 * i, a); stg256(d + 32 * (i + stride), b); stg256(d + 32 * (i + 2 * stride), c);
+    stg256(d + 32 * (i + 3 * stride), e);
+  }
+  for (; i < n32; i += stride) stg256(d + 32 * i, ldg256(s + 32 * i));
+}
+// in-place swap of R-byte blocks k <-> rev(k) with 32-byte vectors
+template <int R, int U>
+__global__ void __launch_bounds__(256) blk_swap256(char* a, int lb) {
+  constexpr int G = R / 32 < 32 ? R / 32 : 32;
+  constexpr int VPL = R / 32 / G;
+  constexpr int BPW = 32 / G;
+  const uint64_t nb = 1ull << lb;
+  const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t k0 = warp * BPW * U; k0 < nb; k0 += nwarps * BPW * U) {
+    u8v v[U][VPL], w[U][VPL];
+    bool act[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = k0 + u * BPW + sub, r = __brevll(k) >> (64 - lb);
+      act[u] = k <= r;
+      if (act[u]) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          v[u][j] = ldp256(a + k * R + (j * G + gl) * 32);
+          w[u][j] = ldp256(a + r * R + (j * G + gl) * 32);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = k0 + u * BPW + sub, r = __brevll(k) >> (64 - lb);
+      if (act[u]) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          stg256(a + r * R + (j * G + gl) * 32, v[u][j]);
+          stg256(a + k * R + (j * G + gl) * 32, w[u][j]);
+        }
+      }
+    }
+  }
+}
+
 // each CTA copies one contiguous chunk of nv / gridDim vectors
 __global__ void __launch_bounds__(256) copy_chunk(const uint4* s, uint4* d, uint64_t nv) {
   const uint64_t per = nv / gridDim.x;
@@ -337,6 +407,19 @@ int main() {
       double t = time_ms([&] { copy_chunk<<<sms * cps, 256>>>((const uint4*)s, (uint4*)d, nv); }, 15);
       printf("{\"bytes\": %llu, \"chunk_ctas_per_sm\": %d, \"chunk_copy_gbs\": %.1f}\n",
              (unsigned long long)bytes, cps, 2.0 * bytes / t / 1e6);
+    }
+    {
+      double t0 = time_ms([&] { copy_lin256<<<sms * 4, 256>>>(s, d, bytes / 32); }, 15);
+      int lb512 = 0, lb1k = 0;
+      while ((512ull << (lb512 + 1)) <= bytes) ++lb512;
+      while ((1024ull << (lb1k + 1)) <= bytes) ++lb1k;
+      double t1 = time_ms([&] { blk_swap256<512, 2><<<sms * 8, 256>>>(d, lb512); }, 15);
+      double t2 = time_ms([&] { blk_swap<512, 4><<<sms * 8, 256>>>(d, lb512); }, 15);
+      double t3 = time_ms([&] { blk_swap256<1024, 2><<<sms * 8, 256>>>(d, lb1k); }, 15);
+      printf("{\"bytes\": %llu, \"copy256_gbs\": %.1f, \"swap256_512_gbs\": %.1f, "
+             "\"swap128_512_gbs\": %.1f, \"swap256_1024_gbs\": %.1f}\n",
+             (unsigned long long)bytes, 2.0 * bytes / t0 / 1e6, 2.0 * bytes / t1 / 1e6,
+             2.0 * bytes / t2 / 1e6, 2.0 * bytes / t3 / 1e6);
     }
     run_bulk<512, 4>(s, d, bytes, sms, 16);
     run_bulk<512, 8>(s, d, bytes, sms, 16);

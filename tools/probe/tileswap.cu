@@ -63,13 +63,57 @@ __global__ void __launch_bounds__(NT) tile_swap(char* a, const uint32_t* ys, int
   }
 }
 
+struct u8v { unsigned v[8]; };
+__device__ __forceinline__ u8v ldp256(const void* p) {
+  u8v r;
+  asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                 "=r"(r.v[6]), "=r"(r.v[7]) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg256(void* p, const u8v& a) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.v[0]), "r"(a.v[1]),
+               "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]) : "memory");
+}
+// the same pattern with 32-byte accesses
+template <int R, int ROWS, int NT>
+__global__ void __launch_bounds__(NT) tile_swap256(char* a, const uint32_t* ys, int npairs, int m,
+                                                  uint64_t stride) {
+  constexpr int CPR = R / 32;
+  constexpr int VPT = ROWS * CPR / NT;
+  static_assert(VPT >= 1 && ROWS * CPR % NT == 0, "split");
+  for (int p = blockIdx.x; p < npairs; p += gridDim.x) {
+    const uint64_t y = ys[p];
+    const uint64_t ry = m ? (__brevll(y) >> (64 - m)) : 0;
+    u8v v0[VPT], v1[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int id = j * NT + threadIdx.x;
+      const int row = id / CPR, c = id % CPR;
+      v0[j] = ldp256(a + row * stride + y * R + c * 32);
+      if (ry != y) v1[j] = ldp256(a + row * stride + ry * R + c * 32);
+    }
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int id = j * NT + threadIdx.x;
+      const int row = id / CPR, c = id % CPR;
+      if (ry != y) {
+        stg256(a + row * stride + ry * R + c * 32, v0[j]);
+        stg256(a + row * stride + y * R + c * 32, v1[j]);
+      } else {
+        stg256(a + row * stride + y * R + c * 32, v0[j]);
+      }
+    }
+  }
+}
+
 static uint32_t revb(uint32_t v, int m) {
   uint32_t r = 0;
   for (int i = 0; i < m; ++i) r |= ((v >> i) & 1u) << (m - 1 - i);
   return r;
 }
 
-template <int R, int NT>
+template <int R, int NT, bool W256 = false>
 void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
   constexpr int ROWS = 64;
   const uint64_t stride = total / ROWS;
@@ -93,18 +137,25 @@ void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
     return level(x) < level(y);
   });
   const std::vector<uint32_t>* orders[3] = {&asc, &shuf, &lvl};
+  int occ = 0;
+  if constexpr (W256) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_swap256<R, ROWS, NT>, NT, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_swap<R, ROWS, NT>, NT, 0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int o = 0; o < 3; ++o) {
+  for (int o = 2; o < 3; ++o) {
     cudaMemcpy(d_ys, orders[o]->data(), orders[o]->size() * 4, cudaMemcpyHostToDevice);
     const int np = (int)orders[o]->size();
     const int grid = sms * ctas_per_sm;
-    for (int w = 0; w < 3; ++w) tile_swap<R, ROWS, NT><<<grid, NT>>>(a, d_ys, np, m, stride);
+    auto launch = [&]() {
+      if constexpr (W256) tile_swap256<R, ROWS, NT><<<grid, NT>>>(a, d_ys, np, m, stride);
+      else tile_swap<R, ROWS, NT><<<grid, NT>>>(a, d_ys, np, m, stride);
+    };
+    for (int w = 0; w < 3; ++w) launch();
     std::vector<float> ts;
     for (int r = 0; r < 15; ++r) {
       cudaEventRecord(e0);
-      tile_swap<R, ROWS, NT><<<grid, NT>>>(a, d_ys, np, m, stride);
+      launch();
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -114,9 +165,9 @@ void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
     std::sort(ts.begin(), ts.end());
     const uint64_t moved = 2 * (uint64_t)ROWS * R * n;
     printf("{\"bytes\": %llu, \"R\": %d, \"m\": %d, \"order\": %d, \"nt\": %d, \"ctas_per_sm\": %d, "
-           "\"gbs\": %.1f, \"best_gbs\": %.1f}\n",
-           (unsigned long long)total, R, m, o, NT, ctas_per_sm, moved / ts[ts.size() / 2] / 1e6,
-           moved / ts[0] / 1e6);
+           "\"w256\": %d, \"occ\": %d, \"gbs\": %.1f, \"best_gbs\": %.1f}\n",
+           (unsigned long long)total, R, m, o, NT, ctas_per_sm, (int)W256, occ,
+           moved / ts[ts.size() / 2] / 1e6, moved / ts[0] / 1e6);
   }
 }
 
@@ -129,10 +180,13 @@ int main() {
     cudaMalloc(&a, total);
     cudaMalloc(&ys, (total / 64 / 256) * 4 + 1024);
     cudaMemset(a, 3, total);
-    run<256, 256>(a, ys, total, sms, 4);
     run<512, 256>(a, ys, total, sms, 4);
-    run<512, 512>(a, ys, total, sms, 2);
-    run<1024, 512>(a, ys, total, sms, 2);
+    run<512, 128, true>(a, ys, total, sms, 8);
+    run<512, 128, true>(a, ys, total, sms, 3);
+    run<512, 128, true>(a, ys, total, sms, 2);
+    run<512, 128>(a, ys, total, sms, 8);
+    run<512, 256, true>(a, ys, total, sms, 2);
+    run<512, 512, true>(a, ys, total, sms, 1);
     cudaFree(a);
     cudaFree(ys);
   }
