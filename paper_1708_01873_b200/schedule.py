@@ -5,8 +5,10 @@ A schedule of width b lists every (i, rev i) with i < rev i; swapping the
 pairs in any order IS the permutation.  generate_swap_schedule /
 cached_schedule return the reference's pair array in its emission order
 (_fill_pairs, src/schedule.py:53-91), generated on the device by
-bitrev_swap_schedule (one thread per pair, no host loop), as a read-only
-(count, 2) int64 CUDA tensor.  apply_schedule replays a complete schedule
+bitrev_swap_schedule (one thread per pair, no host loop), as a (count, 2)
+int64 CUDA tensor.  save_schedule / load_schedule keep the reference's file
+format (src/schedule.py:133-158): the 8-byte magic, one width byte, then the
+pairs as little-endian u64.  apply_schedule replays a complete schedule
 with the tile kernels (its pairs need not even be materialised), an explicit
 disjoint list with the pair kernel, and a list whose pairs share indices in
 list order, exactly like _apply_pairs (src/schedule.py:100-107).
@@ -23,6 +25,7 @@ from . import _core, _lib
 from ._core import as_tensor
 
 SCHEDULE_MAX_BITS = 26
+SCHEDULE_MAGIC = b"BRSCHD01"  # schedule file header (src/schedule.py:20)
 
 
 def swap_count(b: int) -> int:
@@ -125,3 +128,36 @@ def apply_schedule(array, schedule: SwapSchedule) -> None:
     with torch.cuda.device(a.device):
         _lib.call(name, a.data_ptr(), pairs.data_ptr(), pairs.shape[0], _core.elem_bytes(a),
                   _core._stream_ptr(a.device))
+
+
+def save_schedule(schedule: SwapSchedule, path) -> None:
+    """Write the schedule in the reference's format: magic, width byte, pairs
+    as little-endian u64 (src/schedule.py:133-138)."""
+    p = schedule.pairs
+    arr = p.detach().cpu().numpy() if isinstance(p, torch.Tensor) else np.asarray(p)
+    with open(path, "wb") as fh:
+        fh.write(SCHEDULE_MAGIC)
+        fh.write(bytes([schedule.b]))
+        fh.write(np.ascontiguousarray(arr, dtype="<u8").tobytes())
+
+
+def load_schedule(path) -> SwapSchedule:
+    """Read a schedule file (src/schedule.py:141-158): the magic and the pair
+    count (swap_count of the stored width) are checked; the pairs come back as
+    a read-only host int64 array, replayed as an explicit list."""
+    with open(path, "rb") as fh:
+        head = fh.read(len(SCHEDULE_MAGIC))
+        if head != SCHEDULE_MAGIC:
+            raise ValueError(f"{path}: bad magic {head!r}")
+        wb = fh.read(1)
+        if len(wb) != 1:
+            raise ValueError(f"{path}: truncated header")
+        body = fh.read()
+    b = wb[0]
+    words = np.frombuffer(body, dtype="<u8").astype(np.int64)
+    want = swap_count(b) if b >= 1 else 0
+    if words.size != 2 * want:
+        raise ValueError(f"{path}: expected {want} pairs for width {b}, found {words.size // 2}")
+    pairs = words.reshape(-1, 2)
+    pairs.setflags(write=False)
+    return SwapSchedule(b, pairs)

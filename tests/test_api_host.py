@@ -244,3 +244,23 @@ def test_complete_schedule_is_lazy():
     assert s._pairs is None  # nothing materialised until .pairs is read
     e = br.SwapSchedule(3, np.array([[1, 4], [3, 6]]))
     assert not e.complete and len(e) == 2
+
+
+def test_schedule_file_format(tmp_path):
+    """save_schedule / load_schedule: the reference's BRSCHD01 layout
+    (/root/reference/pkg/tests/test_schedule.py:135-167), on an explicit
+    host schedule (generation needs the device)."""
+    pairs = np.array([[2, 4], [1, 8], [3, 12], [5, 10], [7, 14], [11, 13]], dtype=np.int64)
+    s = br.SwapSchedule(4, pairs)
+    path = tmp_path / "s.bin"
+    br.save_schedule(s, path)
+    raw = path.read_bytes()
+    assert raw[:8] == b"BRSCHD01" and raw[8] == 4 and len(raw) == 9 + 16 * 6
+    back = br.load_schedule(path)
+    assert back.b == 4 and np.array_equal(back.pairs, pairs) and not back.pairs.flags.writeable
+    (tmp_path / "junk.bin").write_bytes(b"NOTMAGIC" + bytes([3]))
+    with pytest.raises(ValueError, match="magic"):
+        br.load_schedule(tmp_path / "junk.bin")
+    (tmp_path / "cut.bin").write_bytes(raw[:-16])
+    with pytest.raises(ValueError, match="expected"):
+        br.load_schedule(tmp_path / "cut.bin")

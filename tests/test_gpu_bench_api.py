@@ -159,3 +159,18 @@ def test_tune_tiles(cuda, E, inplace):
         finally:
             br.set_tile_bits(E, inplace, before[0])
             br.set_tile_path(E, inplace, before[1])
+
+
+@pytest.mark.parametrize("b", [1, 5, 10])
+def test_schedule_file_round_trip(cuda, tmp_path, b):
+    s = br.generate_swap_schedule(b)
+    path = tmp_path / f"sched{b}.bin"
+    br.save_schedule(s, path)
+    back = br.load_schedule(path)
+    assert back.b == b and np.array_equal(back.pairs, s.pairs.cpu().numpy())
+    raw = np.frombuffer(path.read_bytes()[9:], dtype="<u8").reshape(-1, 2)
+    assert hashlib.sha256(raw.astype("<i8").tobytes()).hexdigest() == GOLD["sha256"][str(b)]
+    x = torch.randint(0, 1 << 30, (1 << b,), device=cuda, dtype=torch.int64)
+    a = x.clone()
+    br.apply_schedule(a, back)
+    assert torch.equal(a, br.oracle_permute(x, b))
