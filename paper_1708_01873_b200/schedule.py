@@ -115,7 +115,7 @@ def apply_schedule(array, schedule: SwapSchedule) -> None:
     if not a.is_contiguous():
         raise ValueError("apply_schedule with explicit pairs needs a contiguous array")
     p = schedule.pairs
-    pairs = (torch.from_numpy(np.ascontiguousarray(p, dtype=np.int64)) if isinstance(p, np.ndarray)
+    pairs = (torch.from_numpy(np.array(p, dtype=np.int64)) if isinstance(p, np.ndarray)
              else p.to(torch.int64)).to(a.device).contiguous()
     if pairs.numel() == 0:
         return
