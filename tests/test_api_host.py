@@ -264,3 +264,27 @@ def test_schedule_file_format(tmp_path):
     (tmp_path / "cut.bin").write_bytes(raw[:-16])
     with pytest.raises(ValueError, match="expected"):
         br.load_schedule(tmp_path / "cut.bin")
+
+
+def test_scalar_index_helpers():
+    """rev_bytetable / count_leading_zeros / xor_next (src/bits.py:59-113),
+    with the reference's known answers (pkg/tests/test_bits.py:137-142)."""
+    assert br.xor_next(br.RevPair(0, 0), 3) == br.RevPair(1, 4)
+    assert br.xor_next(br.RevPair(3, 6), 3) == br.RevPair(4, 1)
+    rng = np.random.default_rng(7)
+    for b in range(1, 49):
+        for i in rng.integers(0, 1 << b, 20, dtype=np.uint64).tolist():
+            assert br.rev_bytetable(int(i), b) == br.rev_naive(int(i), b)
+    state = br.RevPair(0, 0)
+    for i in range(1, 1 << 8):
+        state = br.xor_next(state, 8)
+        assert state == (i, br.rev_naive(i, 8))
+    with pytest.raises(ValueError):
+        br.xor_next(br.RevPair(255, 255), 8)
+    assert br.count_leading_zeros(1) == 63 and br.count_leading_zeros(1 << 63) == 0
+    with pytest.raises(ValueError):
+        br.count_leading_zeros(0)
+    with pytest.raises(ValueError):
+        br.count_leading_zeros(1 << 64)
+    with pytest.raises(ValueError):
+        br.rev_bytetable(8, 3)

@@ -174,3 +174,9 @@ def test_schedule_file_round_trip(cuda, tmp_path, b):
     a = x.clone()
     br.apply_schedule(a, back)
     assert torch.equal(a, br.oracle_permute(x, b))
+
+
+def test_audit_swap_counts(cuda):
+    assert br.audit_swap_counts(14) == {b: True for b in range(1, 15)}
+    with pytest.raises(ValueError):
+        br.audit_swap_counts(27)
