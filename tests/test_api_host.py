@@ -288,3 +288,16 @@ def test_scalar_index_helpers():
         br.count_leading_zeros(1 << 64)
     with pytest.raises(ValueError):
         br.rev_bytetable(8, 3)
+
+
+def test_every_reference_export_exists():
+    """Drop-in: every name in the reference package's __all__
+    (tests/golden/reference_exports.json, read from
+    /root/reference/pkg/src/bitrev/__init__.py) is exported here too."""
+    import json
+    from pathlib import Path
+
+    names = json.loads((Path(__file__).parent / "golden" / "reference_exports.json").read_text())["names"]
+    missing = [n for n in names if not hasattr(br, n)]
+    assert not missing, missing
+    assert set(names) <= set(br.__all__)
