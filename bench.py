@@ -890,8 +890,12 @@ def main():
     if args.workload == "cfg5" and not args.p2p:
         phases = cfg5_phases(torch, dist, sharded, x, b, world)
         if world > 1 and args.dist_backend == "nccl" and not args.no_fused:
+            gc.collect()
+            torch.cuda.empty_cache()  # the symmetric heap is a separate allocation
             fused = fused_p2p_companion(torch, dist, sharded, x, b, rank, world,
                                         max(3, min(args.steps, 10)), stream)
+            gc.collect()
+            torch.cuda.empty_cache()
 
     # same-harness reference: torch copy_ of the same bytes with the same
     # flush protocol (a device copy moves 2*n*E bytes, like one permutation)
