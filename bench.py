@@ -403,14 +403,34 @@ def run_reference_arm(args):
 
 
 def single_thread_methods(workload, budget_s=20.0):
-    """The reference's single-thread methods on the same array:
-    COBRA (q = default_cobra_q), semi-recursive and recursive, once each, GB/s."""
+    """The reference's single-thread methods on the same array.
+
+    Up to 2 GiB per side: COBRA (q = default_cobra_q), semi-recursive and
+    recursive through the C port, once each.  For config 3 (2^30 elements):
+    the reference package's own cobra_out_of_place, the method BASELINE.md
+    times at that size (src/permutations.py:293-308), once, after a small
+    JIT warm-up.  GB/s."""
     from oracle import oracle as orc
 
     b, dtname, E, inplace, batch, _ = WORKLOADS[workload]
+    np_dt = NP_DTYPES[dtname]
+    if workload.startswith("cfg3"):
+        ref = load_reference_package()
+        if ref is None:
+            return None
+        small_a, small_d = _host_array(1 << 12, np_dt), np.empty(1 << 12, dtype=np_dt)
+        ref.cobra_out_of_place(small_a, small_d, ref.CobraConfig(6), 12)  # JIT compile
+        a = _host_array(1 << b, np_dt)
+        d = np.empty_like(a)
+        t0 = time.perf_counter()
+        ref.cobra_out_of_place(a, d, ref.CobraConfig(6), b)
+        dt = time.perf_counter() - t0
+        return {"unit": "GB/s", "threads": 1, "kind": "reference",
+                "values": {"cobra_out_of_place": round(2 * a.nbytes / dt / 1e9, 3)},
+                "seconds": round(dt, 2)}
     if workload.startswith("cfg4") or workload == "cfg5" or (1 << b) * E > (2 << 30):
         return None
-    a = _host_array(1 << b, NP_DTYPES[dtname])
+    a = _host_array(1 << b, np_dt)
     q = min(b // 2, 6)
     runs = [("cobra_in_place" if inplace else "cobra_out_of_place",
              (lambda: orc.c_cobra_inplace(a, b, q)) if inplace else (lambda: orc.c_cobra_oop(a, b, q))),
