@@ -111,6 +111,9 @@ def sharded_bitrev(local: torch.Tensor, b: int, group=None, *, chunks: int = 1,
         # shards this small gain nothing from overlap
         chunks = 1
     kb = chunks.bit_length() - 1
+    if (pack is None or unpack is None) and not local.is_cuda:
+        raise ValueError("sharded_bitrev runs its local steps on the GPU: the shard must be a "
+                         "CUDA tensor")
     pack = pack or _pack
     unpack = unpack or _unpack
     timed = phases is not None and local.is_cuda

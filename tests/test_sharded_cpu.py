@@ -117,3 +117,9 @@ def test_sharded_bitrev_gloo(world, chunks, b):
     for p in procs:
         p.join(timeout=60)
     assert results == {r: True for r in range(world)}
+
+
+def test_sharded_bitrev_rejects_host_shards():
+    """No CPU path: the default local steps need a CUDA shard."""
+    with pytest.raises(ValueError, match="CUDA"):
+        sharded.sharded_bitrev(torch.zeros(1 << 10, dtype=torch.int64), 10)
