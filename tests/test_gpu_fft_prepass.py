@@ -108,3 +108,16 @@ def test_validation(cuda):
         br.bitrev_dit_prepass(z, 14, 9)  # complex64 tiles fuse at most 7 stages
     assert br.max_fused_stages(14, 8) == 7 and br.max_fused_stages(14, 16) == 6
     assert br.max_fused_stages(11, 16) == 11
+
+
+@pytest.mark.parametrize("stages", [2, 5, 7])
+def test_cfg4_shape_batched_complex64(cuda, stages):
+    """cfg4's shape (rows of 2^16 complex64, here 16 of them) through the
+    256-byte-piece tiles (2-6 stages) and the radix-8 drain (7 stages), forward
+    and inverse, every row against the float64 restatement."""
+    b = 16
+    x = rand_complex((16, 1 << b), torch.complex64, 40 + stages)
+    for inverse in (False, True):
+        got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages, inverse=inverse)
+        ref = np.stack([dit_reference(r, b, stages, inverse) for r in x])
+        check(got, ref, torch.complex64, stages)
