@@ -1,4 +1,6 @@
 # E=8 in place: register pairs (path 0) vs 2-CTA cluster pairs (path 6) at 256 / 128 threads
+# Historical record: the knob this A/B switched was removed from the library after
+# the measurement (result under profiles/r02_*); rerunning measures the default twice.
 O=gpurun_out
 : > $O/ip_cluster_nt_ab.jsonl
 for r in 1 2 3; do
