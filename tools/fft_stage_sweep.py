@@ -33,7 +33,7 @@ def t(fn, reps=20):
     return 2 * x.numel() * E * reps / (s.elapsed_time(e) / 1e3) / 1e9
 
 
-for stages in (0, 1, 2, 3, 4, 5, 6, 7) if E == 8 else (0, 1, 2, 4, 6):
+for stages in (0, 1, 2, 3, 4, 5, 6, 7) if E == 8 else (0, 1, 2, 3, 4, 5, 6):
     gbs = t(lambda: _lib.call("bitrev_dit_prepass", x.data_ptr(), y.data_ptr(), b, E, rows,
                               1 << b, 1 << b, stages, 0, st))
     print(f"{tag} fft rect stages={stages}: {gbs:.0f} GB/s")
