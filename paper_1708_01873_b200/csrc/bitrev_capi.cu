@@ -4,12 +4,17 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <map>
+#include <memory>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "bitrev_b200.h"
 #include "bitrev_kernels.cuh"
@@ -916,6 +921,166 @@ cudaError_t copy_split(void* dst, const void* src, size_t bytes, cudaMemcpyKind 
   return cudaSuccess;
 }
 
+// ---------------------------------------------------------------------------
+// Pageable host memory (numpy arrays): the runtime's own pageable copies run
+// ~15 GB/s for the whole round trip (tools/numpy_path_probe.py).  Instead the
+// bytes are staged through a small ring of pinned bounce buffers: host
+// threads copy chunk k+1 into a bounce slot while the DMA engine moves chunk
+// k, in both directions.
+
+// Fixed pool of host threads for parallel memcpy (never destroyed: its
+// threads are detached and live as long as the process).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* pool = new CopyPool();
+    return *pool;
+  }
+  void copy(void* dst, const void* src, size_t n) {
+    if (n < (size_t(4) << 20) || nworkers_ == 0) {
+      memcpy(dst, src, n);
+      return;
+    }
+    auto j = std::make_shared<Job>();
+    j->dst = static_cast<char*>(dst);
+    j->src = static_cast<const char*>(src);
+    j->n = n;
+    const size_t parts = size_t(nworkers_ + 1) * 2;
+    j->piece = ((n + parts - 1) / parts + 4095) & ~size_t(4095);
+    j->npieces = (n + j->piece - 1) / j->piece;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = j;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work(*j);  // the caller takes pieces too
+    while (j->done.load(std::memory_order_acquire) < j->npieces) std::this_thread::yield();
+  }
+
+ private:
+  struct Job {
+    char* dst = nullptr;
+    const char* src = nullptr;
+    size_t n = 0, piece = 0, npieces = 0;
+    std::atomic<size_t> next{0}, done{0};
+  };
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    nworkers_ = (int)std::min(7u, hw > 1 ? hw - 1 : 0u);
+    for (int i = 0; i < nworkers_; ++i) std::thread([this] { loop(); }).detach();
+  }
+  static void work(Job& j) {
+    for (size_t k; (k = j.next.fetch_add(1, std::memory_order_relaxed)) < j.npieces;) {
+      const size_t off = k * j.piece, len = std::min(j.piece, j.n - off);
+      memcpy(j.dst + off, j.src + off, len);
+      j.done.fetch_add(1, std::memory_order_release);
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::shared_ptr<Job> j;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        j = job_;
+      }
+      work(*j);
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::shared_ptr<Job> job_;
+  uint64_t gen_ = 0;
+  int nworkers_ = 0;
+};
+
+// Pinned bounce ring of the calling thread (per device, lazily allocated,
+// never freed: see PipeRes).
+constexpr int kBounceSlots = 3;
+constexpr size_t kBounceBytes = size_t(64) << 20;
+struct Bounce {
+  bool ok = false;
+  char* slot[kBounceSlots] = {};
+  cudaEvent_t ev[kBounceSlots] = {};
+};
+
+cudaError_t bounce_ring(Bounce** out) {
+  thread_local Bounce rings[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  Bounce& r = rings[dev];
+  if (!r.ok) {
+    for (int i = 0; i < kBounceSlots; ++i) {
+      void* p = nullptr;
+      if ((e = cudaHostAlloc(&p, kBounceBytes, cudaHostAllocPortable)) != cudaSuccess) return e;
+      r.slot[i] = static_cast<char*>(p);
+      if ((e = cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    r.ok = true;
+  }
+  *out = &r;
+  return cudaSuccess;
+}
+
+bool pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // older drivers report unregistered memory as an error
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// host (pageable) -> device on st through the bounce ring; returns once the
+// last chunk's DMA is enqueued (the slots are guarded by their events)
+cudaError_t h2d_staged(void* dev, const void* host, size_t bytes, cudaStream_t st) {
+  Bounce* r = nullptr;
+  cudaError_t e = bounce_ring(&r);
+  if (e != cudaSuccess) return e;
+  for (size_t off = 0, i = 0; off < bytes; off += kBounceBytes, ++i) {
+    const int s = (int)(i % kBounceSlots);
+    const size_t n = std::min(kBounceBytes, bytes - off);
+    if ((e = cudaEventSynchronize(r->ev[s])) != cudaSuccess) return e;  // slot's last DMA done
+    CopyPool::get().copy(r->slot[s], static_cast<const char*>(host) + off, n);
+    if ((e = cudaMemcpyAsync(static_cast<char*>(dev) + off, r->slot[s], n, cudaMemcpyHostToDevice,
+                             st)) != cudaSuccess)
+      return e;
+    if ((e = cudaEventRecord(r->ev[s], st)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// device -> host (pageable) after st's prior work, through the bounce ring;
+// returns when every byte is in host memory
+cudaError_t d2h_staged(void* host, const void* dev, size_t bytes, cudaStream_t st) {
+  Bounce* r = nullptr;
+  cudaError_t e = bounce_ring(&r);
+  if (e != cudaSuccess) return e;
+  const size_t nchunks = (bytes + kBounceBytes - 1) / kBounceBytes;
+  auto issue = [&](size_t i) -> cudaError_t {
+    const int s = (int)(i % kBounceSlots);
+    const size_t off = i * kBounceBytes, n = std::min(kBounceBytes, bytes - off);
+    cudaError_t r2 = cudaMemcpyAsync(r->slot[s], static_cast<const char*>(dev) + off, n,
+                                     cudaMemcpyDeviceToHost, st);
+    return r2 != cudaSuccess ? r2 : cudaEventRecord(r->ev[s], st);
+  };
+  for (size_t i = 0; i < nchunks && i < (size_t)kBounceSlots; ++i)
+    if ((e = issue(i)) != cudaSuccess) return e;
+  for (size_t i = 0; i < nchunks; ++i) {
+    const int s = (int)(i % kBounceSlots);
+    const size_t off = i * kBounceBytes, n = std::min(kBounceBytes, bytes - off);
+    if ((e = cudaEventSynchronize(r->ev[s])) != cudaSuccess) return e;
+    CopyPool::get().copy(static_cast<char*>(host) + off, r->slot[s], n);
+    if (i + kBounceSlots < nchunks && (e = issue(i + kBounceSlots)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 // A blocking host-buffer call's copy on stream st, split over st and the
 // thread's aux stream; st continues only after both halves.
 cudaError_t copy_split_on(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
@@ -1129,11 +1294,13 @@ int bitrev_oop_host(const void* host_src, void* host_dst, int b, int elem_bytes,
     dev_dst = static_cast<char*>(own) + bytes;
   }
   const int64_t n = int64_t(1) << b;
-  cudaError_t e = copy_split_on(dev_src, host_src, bytes, cudaMemcpyHostToDevice, st);
+  cudaError_t e = pageable(host_src) ? h2d_staged(dev_src, host_src, bytes, st)
+                                     : copy_split_on(dev_src, host_src, bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     rc = bitrev_oop(dev_src, dev_dst, b, elem_bytes, batch, n, n, stream);
     if (rc == BITREV_OK) {
-      e = copy_split_on(host_dst, dev_dst, bytes, cudaMemcpyDeviceToHost, st);
+      e = pageable(host_dst) ? d2h_staged(host_dst, dev_dst, bytes, st)
+                             : copy_split_on(host_dst, dev_dst, bytes, cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) rc = (int)e;
     }
   } else {
@@ -1159,11 +1326,14 @@ int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void
     dev_buf = own;
   }
   const int64_t n = int64_t(1) << b;
-  cudaError_t e = copy_split_on(dev_buf, host_a, bytes, cudaMemcpyHostToDevice, st);
+  const bool pg = pageable(host_a);
+  cudaError_t e = pg ? h2d_staged(dev_buf, host_a, bytes, st)
+                     : copy_split_on(dev_buf, host_a, bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     rc = bitrev_inplace(dev_buf, b, elem_bytes, batch, n, stream);
     if (rc == BITREV_OK) {
-      e = copy_split_on(host_a, dev_buf, bytes, cudaMemcpyDeviceToHost, st);
+      e = pg ? d2h_staged(host_a, dev_buf, bytes, st)
+             : copy_split_on(host_a, dev_buf, bytes, cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) rc = (int)e;
     }
   } else {

@@ -331,3 +331,30 @@ def test_guard_bands_untouched(cuda, E, path):
     if inplace:
         mask[pad:pad + batch * stride].view(batch, stride)[:, :n] = False
     assert torch.equal(buf.view(torch.uint8).view(-1, E)[mask], before.view(torch.uint8).view(-1, E)[mask])
+
+
+@pytest.mark.parametrize("shape,b", [((1 << 25,), 25), ((5, 1 << 20), 20), ((3, 1 << 12), 12)])
+def test_pageable_numpy_staged_copies(cuda, shape, b):
+    """numpy (pageable) arrays go through the pinned bounce ring in 64 MiB
+    chunks with host threads (whole, partial and single chunks), in and out of
+    place, against the CPU oracle."""
+    import numpy as np
+
+    from oracle import oracle as orc
+
+    host = np.random.default_rng(len(shape) + b).integers(0, 1 << 62, (int(np.prod(shape)) * 2,),
+                                                          dtype=np.int64).view(np.complex128)
+    host = host.reshape(shape)
+    want = np.ascontiguousarray(orc.oracle_permute(host, b))
+    dst = np.empty_like(host)
+    if len(shape) == 1:
+        br.cobra_out_of_place(host, dst, br.CobraConfig(6), b)
+    else:
+        br.bitrev_batched(host, b, dst)
+    assert np.array_equal(dst.view(np.int64), want.view(np.int64))
+    a = host.copy()
+    if len(shape) == 1:
+        br.cobra_in_place(a, br.CobraConfig(6), b)
+    else:
+        br.bitrev_batched_inplace(a, b)
+    assert np.array_equal(a.view(np.int64), want.view(np.int64))
