@@ -301,3 +301,28 @@ def test_every_reference_export_exists():
     missing = [n for n in names if not hasattr(br, n)]
     assert not missing, missing
     assert set(names) <= set(br.__all__)
+
+
+def test_csv_edge_cases(tmp_path):
+    """The reference's CSV contract (pkg/tests/test_bench.py:126-170): empty
+    tables, trailing newline, header / short-row / inconsistent-n errors that
+    name the file position, write failures that name the path."""
+    p = tmp_path / "empty.csv"
+    br.write_csv([], p)
+    assert p.read_text() == "method,b,n,replicate,elapsed_s,per_element_s\n"
+    assert br.read_csv(p) == []
+    recs = [br.make_record("xor", 4, i, 1.5e-6 * (i + 1)) for i in range(3)]
+    br.write_csv(recs, p)
+    assert len(p.read_text().splitlines()) == 4 and p.read_text().endswith("\n")
+    with pytest.raises(OSError, match="no/such/dir"):
+        br.write_csv([], "no/such/dir/out.csv")
+    bad = tmp_path / "bad.csv"
+    bad.write_text("a,b,c\n1,2,3\n")
+    with pytest.raises(ValueError, match="header"):
+        br.read_csv(bad)
+    bad.write_text("method,b,n,replicate,elapsed_s,per_element_s\nxor,4,16,0\n")
+    with pytest.raises(ValueError, match=":2"):
+        br.read_csv(bad)
+    bad.write_text("method,b,n,replicate,elapsed_s,per_element_s\nxor,4,99,0,1e-06,6.25e-08\n")
+    with pytest.raises(ValueError, match="99"):
+        br.read_csv(bad)
