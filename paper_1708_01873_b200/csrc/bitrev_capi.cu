@@ -1358,6 +1358,26 @@ int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int
   const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
   const int64_t n = int64_t(1) << b;
   cudaStream_t user = static_cast<cudaStream_t>(stream);
+  {
+    // pageable arrays cannot overlap their copies (the runtime stages them
+    // synchronously): run each through the bounce-ring single call instead
+    bool any_pageable = false;
+    for (int64_t k = 0; k < count && !any_pageable; ++k)
+      any_pageable = pageable(host_src[k]) || pageable(host_dst[k]);
+    if (any_pageable) {
+      for (int64_t k = 0; k < count; ++k) {
+        if (host_src[k] != host_dst[k]) {
+          rc = bitrev_oop_host(host_src[k], host_dst[k], b, elem_bytes, batch,
+                               dev_scratch, dev_scratch ? static_cast<char*>(dev_scratch) + bytes : nullptr,
+                               stream);
+        } else {
+          rc = bitrev_inplace_host(host_dst[k], b, elem_bytes, batch, dev_scratch, stream);
+        }
+        if (rc != BITREV_OK) return rc;
+      }
+      return BITREV_OK;
+    }
+  }
   void* own = nullptr;
   char* slots = static_cast<char*>(dev_scratch);
   cudaError_t e = cudaSuccess;

@@ -64,3 +64,17 @@ def test_host_pipeline(cuda, E, dt, b, batch, count):
     br.bitrev_host_pipeline(seq, b)  # each array permuted twice -> identity
     for p, a in zip(pinned, arrays[:2]):
         assert np.array_equal(p.numpy().view(np.uint8), a.view(np.uint8))
+
+
+def test_host_pipeline_pageable_in_place(cuda):
+    """numpy (pageable) arrays through bitrev_host_pipeline in place take the
+    staged single-call path; a repeated array is permuted twice (identity)."""
+    import paper_1708_01873_b200 as br
+
+    b = 22
+    rng = np.random.default_rng(5)
+    arrays = [rng.integers(0, 1 << 62, 1 << b, dtype=np.int64) for _ in range(2)]
+    keep = [a.copy() for a in arrays]
+    br.bitrev_host_pipeline([arrays[0], arrays[1], arrays[0]], b)
+    assert np.array_equal(arrays[0], keep[0])
+    assert np.array_equal(arrays[1], orc.oracle_permute(keep[1], b))
