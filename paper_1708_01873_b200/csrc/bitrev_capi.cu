@@ -229,7 +229,7 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
                     cudaStream_t st) {
   using T = Tile<E, Q, NT>;
   auto kern = bitrev_oop_tile_kernel<E, Q, NT, false>;
-  if constexpr (E == 16 && Q == 6 && NT == BITREV_TILE_THREADS)
+  if constexpr ((E == 16 && Q == 6 && NT == BITREV_TILE_THREADS) || (E == 8 && Q == 7 && NT == 512))
     if (stream_stores(E, b, batch)) kern = bitrev_oop_tile_kernel<E, Q, NT, true>;
   if constexpr (E == 16 && Q == 5 && NT == BITREV_TILE_THREADS) {
     // complex128 up to 32 MiB per side (the Q5 tier): 4 CTAs/SM (63

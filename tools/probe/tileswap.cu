@@ -113,9 +113,8 @@ static uint32_t revb(uint32_t v, int m) {
   return r;
 }
 
-template <int R, int NT, bool W256 = false>
+template <int R, int NT, bool W256 = false, int ROWS = 64>
 void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
-  constexpr int ROWS = 64;
   const uint64_t stride = total / ROWS;
   int m = 0;
   while (((uint64_t)R << (m + 1)) <= stride) ++m;
@@ -164,9 +163,9 @@ void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
     }
     std::sort(ts.begin(), ts.end());
     const uint64_t moved = 2 * (uint64_t)ROWS * R * n;
-    printf("{\"bytes\": %llu, \"R\": %d, \"m\": %d, \"order\": %d, \"nt\": %d, \"ctas_per_sm\": %d, "
+    printf("{\"bytes\": %llu, \"rows\": %d, \"R\": %d, \"m\": %d, \"order\": %d, \"nt\": %d, \"ctas_per_sm\": %d, "
            "\"w256\": %d, \"occ\": %d, \"gbs\": %.1f, \"best_gbs\": %.1f}\n",
-           (unsigned long long)total, R, m, o, NT, ctas_per_sm, (int)W256, occ,
+           (unsigned long long)total, ROWS, R, m, o, NT, ctas_per_sm, (int)W256, occ,
            moved / ts[ts.size() / 2] / 1e6, moved / ts[0] / 1e6);
   }
 }
@@ -181,12 +180,14 @@ int main() {
     cudaMalloc(&ys, (total / 64 / 256) * 4 + 1024);
     cudaMemset(a, 3, total);
     run<512, 256>(a, ys, total, sms, 4);
-    run<512, 128, true>(a, ys, total, sms, 8);
-    run<512, 128, true>(a, ys, total, sms, 3);
-    run<512, 128, true>(a, ys, total, sms, 2);
-    run<512, 128>(a, ys, total, sms, 8);
-    run<512, 256, true>(a, ys, total, sms, 2);
-    run<512, 512, true>(a, ys, total, sms, 1);
+    run<512, 256, false, 64>(a, ys, total, sms, 2);
+    run<1024, 512, false, 32>(a, ys, total, sms, 2);
+    run<2048, 1024, false, 32>(a, ys, total, sms, 1);
+    run<2048, 512, false, 16>(a, ys, total, sms, 2);
+    run<2048, 1024, false, 16>(a, ys, total, sms, 1);
+    run<4096, 1024, false, 16>(a, ys, total, sms, 1);
+    run<4096, 1024, false, 8>(a, ys, total, sms, 1);
+    run<1024, 256, false, 16>(a, ys, total, sms, 4);
     cudaFree(a);
     cudaFree(ys);
   }
