@@ -792,6 +792,50 @@ def fused_p2p_companion(torch, dist, sharded, x, b, rank, world, steps, stream):
             "checked": "byte-equal to the NCCL result on every rank"}
 
 
+FUSED_TIMEOUT_S = 240.0
+
+
+def guarded_fused_companion(torch, dist, sharded, x, b, rank, world, steps, stream, line):
+    """fused_p2p_companion under a watchdog.  The companion is the only step
+    that allocates symmetric memory and maps peers; if that stalls on some
+    node (a rendezvous that never completes), every rank's timer fires after
+    FUSED_TIMEOUT_S: rank 0 prints the finished line with the companion
+    marked as timed out, and every rank exits 0, so the NCCL measurement is
+    never lost to the companion."""
+    lock = threading.Lock()
+    state = {"done": False}
+
+    def on_timeout():
+        with lock:
+            if state["done"]:
+                return
+            state["done"] = True
+            if rank == 0:
+                line["fused_p2p"] = {"value": None,
+                                     "error": f"timed out after {FUSED_TIMEOUT_S:.0f} s"}
+                print(json.dumps(line), flush=True)
+            sys.stderr.flush()
+            os._exit(0)
+
+    timer = threading.Timer(FUSED_TIMEOUT_S, on_timeout)
+    timer.daemon = True
+    gc.collect()
+    torch.cuda.empty_cache()  # the symmetric heap is a separate allocation
+    timer.start()
+    try:
+        rec = fused_p2p_companion(torch, dist, sharded, x, b, rank, world, steps, stream)
+    except Exception as exc:  # report, keep the line
+        rec = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:300]}
+    with lock:
+        if state["done"]:  # the watchdog already printed and is exiting
+            time.sleep(3600)
+        state["done"] = True
+    timer.cancel()
+    gc.collect()
+    torch.cuda.empty_cache()
+    return rec
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -906,16 +950,9 @@ def main():
     sampler.mark("load1")
 
     # cfg5: per-phase times and all-to-all bandwidth (one round, instrumented)
-    phases = fused = None
+    phases = None
     if args.workload == "cfg5" and not args.p2p:
         phases = cfg5_phases(torch, dist, sharded, x, b, world)
-        if world > 1 and args.dist_backend == "nccl" and not args.no_fused:
-            gc.collect()
-            torch.cuda.empty_cache()  # the symmetric heap is a separate allocation
-            fused = fused_p2p_companion(torch, dist, sharded, x, b, rank, world,
-                                        max(3, min(args.steps, 10)), stream)
-            gc.collect()
-            torch.cuda.empty_cache()
 
     # same-harness reference: torch copy_ of the same bytes with the same
     # flush protocol (a device copy moves 2*n*E bytes, like one permutation)
@@ -992,9 +1029,6 @@ def main():
 
     if world > 1:
         dist.barrier()
-    if rank != 0:
-        dist.destroy_process_group()
-        return 0
 
     avg_launch = statistics.mean(step_s)
     achieved = bytes_local / avg_launch / 1e9
@@ -1056,8 +1090,15 @@ def main():
             line["roofline"]["kernel"] = "bitrev oop tile kernel (2^32 elements on one GPU)"
         if phases is not None:
             line["phases"] = phases
-        if fused is not None:
-            line["fused_p2p"] = fused
+    if (args.workload == "cfg5" and not args.p2p and world > 1 and args.dist_backend == "nccl"
+            and not args.no_fused):
+        # last, because it is the one step that maps peer memory: a watchdog
+        # prints the line without it if the symmetric-memory setup stalls
+        line["fused_p2p"] = guarded_fused_companion(
+            torch, dist, sharded, x, b, rank, world, max(3, min(args.steps, 10)), stream, line)
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args.workload, args.cpu_sample_s)

@@ -85,3 +85,45 @@ def test_cfg5_two_ranks_one_device_gloo(cuda):
     assert d["e2e"]["h2d_bytes_per_step"] == (1 << 23) * 8
     assert d["gpu_launches"] == 3 * (1 + 4)  # per step: one pack, one unpack per round
     assert "TEST SIZE" in d["config"]["workload"]
+
+
+_WATCHDOG = r"""
+import json, sys, time
+sys.path.insert(0, {root!r})
+import torch
+import bench
+bench.FUSED_TIMEOUT_S = {timeout}
+def companion(*a):
+    time.sleep({sleep})
+    return {{"value": 1.0}}
+bench.fused_p2p_companion = companion
+line = {{"metric": "m", "value": 2.0}}
+rec = bench.guarded_fused_companion(torch, None, None, None, 0, 0, 2, 3, None, line)
+print("RETURNED", json.dumps(rec))
+"""
+
+
+def _watchdog_run(timeout, sleep):
+    code = _WATCHDOG.format(root=str(ROOT), timeout=timeout, sleep=sleep)
+    return subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                          timeout=120)
+
+
+def test_fused_companion_watchdog_prints_line_and_exits_0():
+    """A stalled peer-memory setup must not cost the cfg5 line: rank 0's
+    watchdog prints the finished line (companion marked timed out) and the
+    process exits 0."""
+    p = _watchdog_run(timeout=0.5, sleep=30)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1 and "RETURNED" not in p.stdout
+    assert lines[0]["value"] == 2.0
+    assert lines[0]["fused_p2p"]["value"] is None
+    assert "timed out" in lines[0]["fused_p2p"]["error"]
+
+
+def test_fused_companion_watchdog_quiet_when_in_time():
+    p = _watchdog_run(timeout=30, sleep=0)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert _json_lines(p.stdout) == []
+    assert 'RETURNED {"value": 1.0}' in p.stdout
