@@ -19,7 +19,9 @@ words (int32 / int64 views), so NaN payloads and -0.0 are bytes like any other.
   payload bits, signed zeros, infinities) against the CPU oracle;
 * config 4: the full 4096 x 2^16 complex64 batch against the CPU oracle;
 * config 5's plan at 2^31 complex64 over 8 emulated ranks (16 GiB), every
-  element, with the sub-chunked exchange layout.
+  element, with the sub-chunked exchange layout; and at config 5's own size,
+  2^32 complex64 (32 GiB) over 2 / 4 / 8 emulated ranks (pack + rounds +
+  unpack) and 8 ranks of the fused peer-store scatter.
 """
 
 import gc
@@ -177,6 +179,28 @@ def test_cfg5_plan_2p31_complex64_eight_ranks(cuda):
     S = 1 << (b - 3)
     for d, o in enumerate(outs):
         _check_vs_device_oracle(x, o, b - 3, base=d * S, total_bits=b)
+
+
+@pytest.mark.parametrize("G,mode", [(2, "nccl"), (4, "nccl"), (8, "nccl"), (8, "p2p")])
+def test_cfg5_full_size_2p32_complex64(cuda, G, mode):
+    """Config 5 at its BASELINE size: 2^32 complex64 (32 GiB) over G emulated
+    ranks, every element.  "nccl" = the pack kernel with 4 exchange rounds and
+    the per-round unpack (sharded_bitrev's device steps; at G = 2 each shard
+    holds 2^31 elements); "p2p" = the fused scatter into G receive buffers
+    and the unpack (sharded_bitrev_p2p's device steps)."""
+    b = 32
+    _need(cuda, 3 * (8 << b) + (8 << b) // 4)
+    x = _random_bits(1 << b, torch.complex64, cuda)
+    g = G.bit_length() - 1
+    if mode == "nccl":
+        outs = sharded.emulate_sharded(x, b, G, 4)
+    else:
+        outs = sharded.emulate_sharded_p2p(x, b, G)
+    S = 1 << (b - g)
+    for d in range(G):
+        _check_vs_device_oracle(x, outs[d], b - g, base=d * S, total_bits=b)
+        outs[d] = None
+        gc.collect()
 
 
 @pytest.mark.parametrize("E", [4, 8, 16])
