@@ -49,7 +49,7 @@ int default_q(int E, bool inplace) {
 bool q_supported(int E, int q) {
   switch (E) {
     case 4: return q >= 5 && q <= 8;
-    case 8: return q >= 4 && q <= 7;
+    case 8: return q >= 4 && q <= 8;
     case 16: return q >= 3 && q <= 7;
     default: return false;
   }
@@ -562,7 +562,7 @@ int dispatch_oop_rect(int E, int q, const void* src, void* dst, int b, int64_t b
   if (E == EE && q == QX && qz == QZ)                                          \
     return launch_oop_rect<EE, QX, QZ>(src, dst, b, batch, sbs, dbs, st);
   RECT(4, 6, 5) RECT(4, 7, 6) RECT(4, 8, 6)
-  RECT(8, 5, 4) RECT(8, 6, 5) RECT(8, 7, 5)
+  RECT(8, 5, 4) RECT(8, 6, 5) RECT(8, 7, 5) RECT(8, 8, 5)
   RECT(16, 4, 3) RECT(16, 5, 3) RECT(16, 6, 4) RECT(16, 7, 4)
 #undef RECT
   return BITREV_ETILE;
@@ -787,6 +787,23 @@ Tier mid_tier(int E, bool inplace, uint64_t side_bytes) {
 }
 
 uint64_t side_bytes(int E, int b, int64_t batch) { return ((uint64_t)E << b) * (uint64_t)batch; }
+
+// Batched 8-byte rows out of place, rows of 2^13..2^22 elements past the
+// mid-size budget: rectangular tiles with 2 KB destination rows (QX = 8, 64
+// KB tiles) beat the 1 KB default by 1-4 % (cfg4's 4096 x 2^16: +1.5 %);
+// single arrays of 2^23 and up are neutral to 0.3 % either way
+// (tools/rect_e8_rows_sweep.py -> profiles/r02_rect_e8_rows.jsonl,
+// tools/rect_e8_q8_ab.sh -> profiles/r02_rect_e8_q8_ab.jsonl).
+Tier batched_rows_tier(int E, bool inplace, int b, int64_t batch) {
+  Tier t;
+  if (E != 8 || inplace || batch < 2 || b < 13 || b > 22) return t;
+  if (current_q(E, inplace) != default_q(E, inplace)) return t;
+  if (tile_path(E, inplace) != default_path(E, inplace)) return t;
+  if (side_bytes(E, b, batch) <= (32ull << 20)) return t;
+  t.q = 8;
+  t.path = 3;
+  return t;
+}
 
 // In place, rows of 32-128 KB in large batches also take the short-row
 // kernel (a whole row staged in one CTA, 64/128 KB blocks): +6 % (float32,
@@ -1205,7 +1222,8 @@ int bitrev_oop(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
     // configured path first; every miss (shape not instantiated, b too small)
     // falls through to the square register tiles, then to the gather kernel
     int path = tile_path(E, false), q0 = current_q(E, false);
-    const Tier t = mid_tier(E, false, side_bytes(E, b, batch));
+    Tier t = mid_tier(E, false, side_bytes(E, b, batch));
+    if (!t.q) t = batched_rows_tier(E, false, b, batch);
     if (t.q) {
       q0 = t.q;
       path = t.path;

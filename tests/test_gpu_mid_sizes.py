@@ -89,3 +89,36 @@ def test_last_tile_reports_row_and_elementwise_kernels(cuda):
     br.cobra_in_place(y, br.CobraConfig(0), 16)  # 2-byte elements: element-wise kernel
     assert br.last_tile() == (0, -2)
     torch.cuda.synchronize()
+
+
+# batched 8-byte rows out of place (bitrev_capi.cu batched_rows_tier): rows of
+# 2^13..2^22 elements past the 32 MiB budget take 2 KB destination rows
+BATCHED = [
+    (13, 8192, (8, 3)), (16, 64, (4, 0)), (16, 128, (8, 3)), (22, 2, (8, 3)),
+    (23, 2, (7, 3)),       # rows above 2^22: the default
+    (12, 16384, (0, -3)),  # 32 KB rows: the short-row kernel
+]
+
+
+@pytest.mark.parametrize("b,rows,expected", BATCHED)
+def test_batched_rows_tier_and_parity(cuda, b, rows, expected):
+    x = torch.empty((rows, 1 << b), dtype=torch.float64, device=cuda).normal_()
+    x.view(torch.int64)[:, :7] = torch.tensor([0x7FF8000000000001, -1, 0, -(1 << 63), 1, 2, 3])
+    out = br.bitrev_batched(x, b)
+    torch.cuda.synchronize()
+    assert br.last_tile() == expected
+    idx = torch.from_numpy(orc.rev_index_array(b)).to(cuda)
+    assert torch.equal(out.view(torch.int64), x.view(torch.int64).index_select(1, idx))
+
+
+def test_batched_rows_tier_off_with_pinned_knobs(cuda):
+    old = br.get_tile_bits(8, False)
+    br.set_tile_bits(8, False, 6)
+    try:
+        x = torch.empty((128, 1 << 16), dtype=torch.float64, device=cuda).normal_()
+        br.bitrev_batched(x, 16)
+        assert br.last_tile()[0] == 6
+    finally:
+        br.set_tile_bits(8, False, old)
+    br.bitrev_batched(x, 16)
+    assert br.last_tile() == (8, 3)
