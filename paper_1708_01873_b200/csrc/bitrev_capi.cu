@@ -1682,9 +1682,23 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   // layout exchange tips it into issue-bound).  BITREV_B200_FFT_QZ=4|5 forces
   // one shape (A/B runs).
   static const int qz_env = env_int("BITREV_B200_FFT_QZ", 0);
-  const int qx = E == 8 ? 7 : 6;
+  // complex64: 256-element destination rows (QX = 8: two 128-element FFT
+  // blocks per row, radix-8 drain, 64 KB tiles at 1 CTA/SM) against 128-element
+  // rows (QX = 7, 2 CTAs/SM), tools/fft_qx8_ab.sh / fft_qx8_low_ab.sh /
+  // fft_qx8_sizes.py -> profiles/r02_fft_qx8_*: 1 stage +6-14 % at every
+  // shape, 2-5 stages +3-7 % on rows up to 2^18 and neutral (0.997-1.03) on
+  // longer rows and single arrays; 6-7 stages lose 1-3 % (the drain is
+  // issue-bound at one CTA/SM) except on rows of 2^13-2^14 (+7 %).  Launches
+  // below 16 MiB per side keep the smaller tiles (wave quantisation).
+  // BITREV_B200_FFT_QX=7|8 forces a width (A/B runs).
+  static const int qx_env = env_int("BITREV_B200_FFT_QX", 0);
+  const bool wide_ok = E == 8 && stages >= 1 && stages <= 7 && b >= 13;
+  const bool wide_rule = (stages <= 5 || b <= 14) && side_bytes(E, b, batch) >= (16ull << 20);
+  const bool wide = wide_ok && (qx_env == 8 || (qx_env == 0 && wide_rule));
+  const int qx = wide ? 8 : E == 8 ? 7 : 6;
   int qz = 4;
   if (E == 8) qz = qz_env == 4 || qz_env == 5 ? qz_env : (stages >= 2 ? 5 : 4);
+  if (wide) qz = 5;  // the 256-element rows are instantiated with 256-byte source pieces only
   if (stages > qx || b < qx + qz) return BITREV_ESTAGES;
   const bool vec_ok = aligned16(src) && aligned16(dst) && ((src_batch_stride * E) % 16 == 0) &&
                       ((dst_batch_stride * E) % 16 == 0);
@@ -1699,7 +1713,13 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                      \
     return finish_launch();                                                                  \
   }
-  if (E == 8 && qz == 5) {
+  if (wide && qz == 5) {
+    switch (stages) {
+      FFT_LAUNCH(8, 8, 5, 1) FFT_LAUNCH(8, 8, 5, 2) FFT_LAUNCH(8, 8, 5, 3)
+      FFT_LAUNCH(8, 8, 5, 4) FFT_LAUNCH(8, 8, 5, 5) FFT_LAUNCH(8, 8, 5, 6)
+      FFT_LAUNCH(8, 8, 5, 7)
+    }
+  } else if (E == 8 && qz == 5) {
     switch (stages) {
       FFT_LAUNCH(8, 7, 5, 1) FFT_LAUNCH(8, 7, 5, 2) FFT_LAUNCH(8, 7, 5, 3)
       FFT_LAUNCH(8, 7, 5, 4) FFT_LAUNCH(8, 7, 5, 5) FFT_LAUNCH(8, 7, 5, 6)

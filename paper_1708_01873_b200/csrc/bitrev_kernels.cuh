@@ -1576,27 +1576,34 @@ __device__ __forceinline__ void fft_rows_drain_r4(uint4* U, char* dbase, uint64_
 // layout's 16 lanes of a row hit 16 distinct bank slots.
 struct LaneTw8 {
   float2 w16, w32, w64, w128;  // W_16^r, W_32^r, W_64^r (r = ll & 7), W_128^ll
-  __device__ __forceinline__ void load(const float2* tw, int ll) {  // tw = W_128^j, j < 64
+  // tw = W_{2^QX}^j, j < 2^(QX-1); st = 2^(QX-7) maps W_128^k to tw[k * st]
+  __device__ __forceinline__ void load(const float2* tw, int ll, int st = 1) {
     const int r = ll & 7;
-    w16 = tw[r << 3];
-    w32 = tw[r << 2];
-    w64 = tw[r << 1];
-    w128 = tw[ll];
+    w16 = tw[(r << 3) * st];
+    w32 = tw[(r << 2) * st];
+    w64 = tw[(r << 1) * st];
+    w128 = tw[ll * st];
   }
 };
 
 __device__ __forceinline__ int fft8_swz(int x) { return x ^ ((x >> 4) & 7) ^ (((x >> 6) & 1) << 3); }
 
-template <int QZ, int STAGES>
+// QX = 8 (256-element destination rows): each row holds two 128-element
+// FFT blocks (up to 7 stages stay inside a block); the two half-warps of a
+// warp take the two blocks of one row, so the row is read whole before
+// either half overwrites its own block as exchange scratch.
+template <int QZ, int STAGES, int QX = 7>
 __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_t dst_row,
                                                   const LaneTw8& lt, bool inverse) {
-  static_assert(STAGES >= 4 && STAGES <= 7, "radix-8 drain: 4 to 7 stages");
+  static_assert(STAGES >= 1 && STAGES <= 7, "radix-8 drain: 1 to 7 stages");
+  static_assert(QX == 7 || QX == 8, "128-element blocks, one or two per row");
   using C = float2;
-  using T = Rect<8, 7, QZ>;
+  using T = Rect<8, QX, QZ>;
+  constexpr int NB = 1 << (QX - 7);  // 128-element blocks per row
   constexpr int NWARPS = T::THREADS / 32;
-  constexpr int ROWS = 1 << QZ;
+  constexpr int ROWS = (1 << QZ) * NB;  // blocks
   constexpr int PASSES = ROWS / (2 * NWARPS);
-  static_assert(PASSES >= 1 && ROWS % (2 * NWARPS) == 0, "two rows per warp pass");
+  static_assert(PASSES >= 1 && ROWS % (2 * NWARPS) == 0, "two blocks per warp pass");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = lane >> 4, ll = lane & 15;
   auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
@@ -1608,7 +1615,8 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
   auto mulj = [&](C a) { return C{-sg * a.y, sg * a.x}; };  // a * W_4
 #pragma unroll 1
   for (int pass = 0; pass < PASSES; ++pass) {
-    const int z = (warp + pass * NWARPS) * 2 + h;
+    const int zb = (warp + pass * NWARPS) * 2 + h;
+    const int z = zb >> (QX - 7), blk = zb & (NB - 1);
     C v[8];
     // A8 from the staged tile: the lane's 4 chunks 4 ll + c, read from a
     // rotated start so the 8 lanes of a quarter warp cover all 8 bank slots
@@ -1616,7 +1624,7 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
       const int rot = (ll >> 1) & 3;
       uint4 q[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) q[c] = U[sidx(z, 4 * ll + ((c + rot) & 3))];
+      for (int c = 0; c < 4; ++c) q[c] = U[sidx(z, blk * 64 + 4 * ll + ((c + rot) & 3))];
       if (rot & 1) {
         const uint4 t = q[3];
         q[3] = q[2];
@@ -1646,7 +1654,7 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
       v[m] = cadd(v[m], t);
     }
 #pragma unroll
-    for (int g = 0; g < 8; g += 4) {
+    for (int g = 0; g < 8 && STAGES >= 2; g += 4) {
       C t = v[g + 2];
       v[g + 2] = csub(v[g], t);
       v[g] = cadd(v[g], t);
@@ -1654,7 +1662,7 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
       v[g + 3] = csub(v[g + 1], t);
       v[g + 1] = cadd(v[g + 1], t);
     }
-    {
+    if constexpr (STAGES >= 3) {
       C t = v[4];
       v[4] = csub(v[0], t);
       v[0] = cadd(v[0], t);
@@ -1668,7 +1676,7 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
       v[7] = csub(v[3], t);
       v[3] = cadd(v[3], t);
     }
-    C* row = reinterpret_cast<C*>(U) + (size_t)z * 128;
+    C* row = reinterpret_cast<C*>(U) + (size_t)z * (128 * NB) + blk * 128;
     __syncwarp();  // every lane of the row has read its staged chunks
 #pragma unroll
     for (int m = 0; m < 8; ++m) row[fft8_swz(8 * ll + m)] = v[m];
@@ -1678,7 +1686,7 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
     for (int m = 0; m < 8; ++m) v[m] = row[fft8_swz(r + 8 * m + 64 * hi)];
     // stages 4-6 (B8): pairs 8, 16, 32 apart
 #pragma unroll
-    for (int m = 0; m < 8; m += 2) bfly(v[m], v[m + 1], lt.w16);
+    for (int m = 0; m < 8 && STAGES >= 4; m += 2) bfly(v[m], v[m + 1], lt.w16);
     if constexpr (STAGES >= 5) {
       const C a = lt.w32, b = mulj(lt.w32);  // W_32^r, W_32^(r+8)
 #pragma unroll
@@ -1709,7 +1717,7 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
       bfly(v[3], v[7], b3);
     }
     // natural store: for each m the row's 16 lanes write 128 contiguous bytes
-    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - QZ)) * dst_row;
+    char* drow = dbase + (uint64_t)(__brev((unsigned)z) >> (32 - QZ)) * dst_row + blk * 1024;
 #pragma unroll
     for (int m = 0; m < 8; ++m) *reinterpret_cast<C*>(drow + (uint64_t)(ll + 16 * m) * 8) = v[m];
     __syncwarp();  // the row is free for the next pass's exchange
@@ -1719,7 +1727,8 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
 // Rectangular-tile FFT pre-pass (bitrev_oop_rect_kernel's load/stage path).
 template <int E, int QX, int QZ, int STAGES>
 __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
-                                  STAGES >= BITREV_FFT_MINB_FROM ? (QZ >= 5 ? 2 : BITREV_FFT_MINB) : 1)
+                                  STAGES >= BITREV_FFT_MINB_FROM && QX <= 7
+                                      ? (QZ >= 5 ? 2 : BITREV_FFT_MINB) : 1)
     bitrev_fft_rect_kernel(FftArgs fa) {
   using T = Rect<E, QX, QZ>;
   using C = typename Cplx<E>::T;
@@ -1754,10 +1763,11 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
   if (t >= a.ntiles) return;
   load(t);
   __syncthreads();  // publish twq
-  constexpr bool kR8 = E == 8 && QX == 7 && STAGES >= BITREV_FFT_R8_FROM && STAGES >= 4;
-  LaneTw<E, QX, kR8 ? 0 : STAGES> lt;
+  constexpr bool kR8 = E == 8 && (QX == 8 || (QX == 7 && STAGES >= BITREV_FFT_R8_FROM && STAGES >= 4));
+  static_assert(QX != 8 || kR8, "256-element rows take the radix-8 drain");
+  LaneTw<E, (QX > 7 ? 7 : QX), kR8 ? 0 : STAGES> lt;
   LaneTw8 lt8;
-  if constexpr (kR8) lt8.load(reinterpret_cast<const float2*>(twq), threadIdx.x & 15);
+  if constexpr (kR8) lt8.load(reinterpret_cast<const float2*>(twq), threadIdx.x & 15, 1 << (QX - 7));
   else lt.load(twq, (threadIdx.x & 31) % ((1 << QX) / 4));
   for (;;) {
     const uint64_t bi = t >> a.m, y = t & mmask;
@@ -1773,8 +1783,8 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) load(tn);
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
-    if constexpr (kR8) fft_rows_drain_r8<QZ, STAGES>(smem, dbase, dst_row, lt8, fa.inverse != 0);
-    else fft_rows_drain_r4<E, QX, QZ, STAGES>(smem, dbase, dst_row, lt, fa.inverse != 0);
+    if constexpr (kR8) fft_rows_drain_r8<QZ, STAGES, QX>(smem, dbase, dst_row, lt8, fa.inverse != 0);
+    else fft_rows_drain_r4<E, (QX > 7 ? 7 : QX), QZ, STAGES>(smem, dbase, dst_row, lt, fa.inverse != 0);
     if (tn >= a.ntiles) break;
     __syncthreads();
     t = tn;

@@ -121,3 +121,19 @@ def test_cfg4_shape_batched_complex64(cuda, stages):
         got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages, inverse=inverse)
         ref = np.stack([dit_reference(r, b, stages, inverse) for r in x])
         check(got, ref, torch.complex64, stages)
+
+
+@pytest.mark.parametrize("b,rows,stages", [(16, 80, 1), (16, 80, 2), (16, 80, 3), (16, 80, 4),
+                                           (16, 80, 5), (16, 80, 6), (14, 128, 6), (14, 128, 7),
+                                           (13, 256, 7), (22, 1, 3)])
+def test_wide_rows_tier_complex64(cuda, b, rows, stages):
+    """complex64 launches of >= 16 MiB take the 256-element destination rows
+    (two FFT blocks per row, radix-8 drain: bitrev_dit_prepass's QX = 8 rule)
+    for 1-5 stages, and for 6-7 stages on rows of 2^13-2^14; the other 6-7
+    stage cases stay on 128-element rows.  Forward and inverse, every row
+    against the float64 restatement."""
+    x = rand_complex((rows, 1 << b), torch.complex64, 70 + stages + b)
+    for inverse in (False, True):
+        got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages, inverse=inverse)
+        ref = np.stack([dit_reference(r, b, stages, inverse) for r in x])
+        check(got, ref, torch.complex64, stages)
