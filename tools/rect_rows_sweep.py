@@ -6,6 +6,7 @@ array of 8 GiB.  Median of 20 back-to-back event-timed launches, interleaved
 rounds.  Measurement probe only.
 
   python tools/rect_rows_sweep.py --E 4 --qx 8 9 > out.jsonl
+  python tools/rect_rows_sweep.py --E 16 --qx 0 7 > out.jsonl   (0 = library default)
 """
 import argparse
 import json
@@ -36,6 +37,7 @@ def main():
     buf = torch.empty(2 * (E << single_b), dtype=torch.uint8, device=dev)
     cases = [(b, 1 << (total_b - b)) for b in args.bits if b <= total_b] + [(single_b, 1)]
     tag = os.environ.get("BITREV_B200_RECT_QZ", "table")
+    default_path = _lib.get_tile_path(E, False)  # qx 0 = the library's default choice
     for rnd in range(args.rounds):
         for b, rows in cases:
             n = rows << b
@@ -45,7 +47,7 @@ def main():
                 x, y = x.view(rows, 1 << b), y.view(rows, 1 << b)
             for q in args.qx:
                 _lib.set_tile_bits(E, False, q)
-                _lib.set_tile_path(E, False, 3)
+                _lib.set_tile_path(E, False, 3 if q else default_path)
                 for _ in range(3):
                     _core.launch_oop(x, y, b)
                 ts = []
