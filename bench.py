@@ -497,6 +497,24 @@ class Flush:
         self.torch.sum(self.r, dim=0, out=self.sink)
 
 
+def kernel_family(chosen, inplace):
+    """Kernel family of a (tile bits, staging path) choice (bitrev_last_tile)."""
+    path = chosen[1]
+    if path == 1:
+        return f"bitrev_ring_kernel (TMA bulk-row ring, Q={chosen[0]})"
+    if path == 2:
+        return f"bitrev_ring_kernel (TMA tensor-map ring, Q={chosen[0]})"
+    if path == 3:
+        return f"bitrev_oop_rect_kernel (QX={chosen[0]})"
+    if path == 6:
+        return f"bitrev_inplace_cluster_kernel (Q={chosen[0]})"
+    if path == -3:
+        return "bitrev_rows_kernel (short rows)"
+    if inplace:
+        return f"bitrev_inplace_tile_kernel (Q={chosen[0]})"
+    return f"bitrev_oop_tile_kernel (Q={chosen[0]})"
+
+
 def time_steps(torch, step, steps, stream, flush=None):
     """Per-step seconds of `steps` steps, each bracketed by CUDA events on
     `stream` (flush, if any, outside the events)."""
@@ -559,6 +577,8 @@ def config_sweep(torch, dev, peak, steps, workloads):
                   "step_ms_all": [round(t * 1e3, 4) for t in ts],
                   "tile_bits": None if w == "cfg4-fft7" else q,
                   "tile_path": None if w == "cfg4-fft7" else path,
+                  "kernel": ("bitrev_fft_rect_kernel" if w == "cfg4-fft7" else
+                             kernel_family((q, path), inplace)),
                   "l2": "flushed before every step" if flush else "inputs larger than L2, no flush",
                   "workload": desc}
         del x, y, flush
@@ -1037,7 +1057,7 @@ def main():
         value = (1 << b) * 2 * E * args.steps / job_time / 1e9
     traffic = load_traffic(args.workload)
     kernel = ("bitrev_fft_rect_kernel" if args.workload == "cfg4-fft7" else
-              "bitrev_inplace_tile_kernel" if inplace else "bitrev oop tile kernel")
+              kernel_family(chosen, inplace))
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": job_time / args.steps * 1e3,

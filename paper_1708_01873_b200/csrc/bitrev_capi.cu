@@ -779,7 +779,15 @@ Tier mid_tier(int E, bool inplace, uint64_t side_bytes) {
   } else if (E == 8 && inplace) {
     if (within(64)) t = {4, 0};
   } else if (E == 16 && !inplace) {
-    if (within(32)) t = {5, 0};
+    // 8-32 MiB per side: Q4 tiles through the TMA tensor ring (96 KB, 2
+    // CTAs/SM).  From DRAM it ties the Q5 register tiles (b = 20: 3264-3282
+    // vs 3256-3280 GB/s; b = 21: -0.9 %); with the array L2-resident it is
+    // +7.5 % (b = 20) / +23 % (b = 21): one TMA instruction per tile instead
+    // of the register path's LDG/STS issue (tools/small_ring_e16_ab.sh ->
+    // profiles/r02_small_ring_e16_ab.jsonl).  Up to 8 MiB the register tiles
+    // stay ahead L2-resident (b = 17/18: -12 % / -4 % for the ring).
+    if (within(8)) t = {5, 0};
+    else if (within(32)) t = {4, 2};
   } else if (E == 16 && inplace) {
     if (within(512)) t = {5, 0};  // single-CTA pairs up to b = 25; clusters from b = 26
   }

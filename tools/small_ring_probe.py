@@ -27,6 +27,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="96")
     ap.add_argument("--reps", type=int, default=60)
+    ap.add_argument("--E", type=int, nargs="+", default=[4, 8, 16])
+    ap.add_argument("--bits", type=int, nargs="+", default=None)
+    ap.add_argument("--cands", nargs="+", default=None,
+                    help="q:path pairs (default: the tier's q with paths 0 and 2)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     w = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -68,19 +72,21 @@ def main():
         torch.cuda.synchronize()
         return s.elapsed_time(e) * 1e3 / (per * replays)
 
-    for E, bits in BITS.items():
-        for b in bits:
+    for E in args.E:
+        cands = ([tuple(int(v) for v in c.split(":")) for c in args.cands] if args.cands
+                 else [(TIER_Q[E], 0), (TIER_Q[E], 2)])
+        for b in (args.bits or BITS[E]):
             x = torch.empty((1 << b) * E, dtype=torch.uint8, device=dev).random_(0, 256).view(DT[E])
             y = torch.empty_like(x)
             nbytes = 2 * x.numel() * E
-            for path in (0, 2):
-                _lib.set_tile_bits(E, False, TIER_Q[E])
+            for q, path in cands:
+                _lib.set_tile_bits(E, False, q)
                 _lib.set_tile_path(E, False, path)
                 fn = lambda: _core.launch_oop(x, y, b)  # noqa: E731
                 fn()
                 used = _lib.last_tile()
                 tf, th = flushed(fn), hot(fn)
-                print(json.dumps({"budget": args.tag, "E": E, "b": b, "path": path, "used": used,
+                print(json.dumps({"budget": args.tag, "E": E, "b": b, "q": q, "path": path, "used": used,
                                   "flushed_us": round(tf, 3), "flushed_gbs": round(nbytes / tf / 1e3, 1),
                                   "hot_us": round(th, 3), "hot_gbs": round(nbytes / th / 1e3, 1)}),
                       flush=True)
