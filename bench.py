@@ -1107,7 +1107,7 @@ def main():
             if phases and "a2a" in phases:
                 line["nvlink_roofline"] = phases["a2a"]
         else:
-            line["roofline"]["kernel"] = "bitrev oop tile kernel (2^32 elements on one GPU)"
+            line["roofline"]["kernel"] = f"{kernel} (2^32 elements on one GPU)"
         if phases is not None:
             line["phases"] = phases
     if (args.workload == "cfg5" and not args.p2p and world > 1 and args.dist_backend == "nccl"
