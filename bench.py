@@ -590,9 +590,10 @@ def config_sweep(torch, dev, peak, steps, workloads):
 def e2e_host(torch, br, x, b, E, inplace, workload, steps, stream):
     """End to end through the public API with host buffers (rank 0's replica).
 
-    e2e: bitrev_host_pipeline over a stream of pinned host arrays (each step =
-    one array: its H2D copy, the permutation and its D2H copy; consecutive
-    steps overlap their copies in opposite directions).  e2e_single: one
+    e2e: bitrev_host_pipeline (cfg4-fft7: dit_prepass_host_pipeline) over a
+    stream of pinned host arrays (each step = one array: its H2D copy, the
+    kernel and its D2H copy; consecutive steps overlap their copies in
+    opposite directions).  e2e_single: one
     blocking reference-style call per array (cobra_in_place /
     cobra_out_of_place / bitrev_batched / bitrev_dit_prepass on a host tensor:
     H2D, kernel, D2H, sync, nothing overlapped).  All host buffers are freed
@@ -609,7 +610,10 @@ def e2e_host(torch, br, x, b, E, inplace, workload, steps, stream):
     def run_pipeline():
         srcs = [hosts[k % nhost] for k in range(reps)]
         dsts = None if houts is None else [houts[k % nhost] for k in range(reps)]
-        br.bitrev_host_pipeline(srcs, b, dsts)
+        if workload == "cfg4-fft7":
+            br.dit_prepass_host_pipeline(srcs, b, 7, dsts)
+        else:
+            br.bitrev_host_pipeline(srcs, b, dsts)
 
     def single_step():
         if workload == "cfg4-fft7":
@@ -622,8 +626,6 @@ def e2e_host(torch, br, x, b, E, inplace, workload, steps, stream):
             br.cobra_out_of_place(hosts[0], houts[0], cfg, b)
 
     plan = ((run_pipeline, reps, "pipe"), (single_step, 1, "single"))
-    if workload == "cfg4-fft7":  # the host pipeline runs the plain permutation
-        plan = ((single_step, 1, "single"),)
     for fn, n_steps, key in plan:
         fn()  # warm (stream/pool creation, page-locking caches)
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -640,8 +642,10 @@ def e2e_host(torch, br, x, b, E, inplace, workload, steps, stream):
                "h2d_bytes_per_step": n_local * E, "d2h_bytes_per_step": n_local * E,
                "ms_per_step": t_step * 1e3}
         if key == "pipe":
-            rec["path"] = (f"bitrev_host_pipeline over {reps} pinned host arrays (public API; "
-                           "per step: H2D + permute + D2H, consecutive steps overlapped)")
+            api = ("dit_prepass_host_pipeline" if workload == "cfg4-fft7" else
+                   "bitrev_host_pipeline")
+            rec["path"] = (f"{api} over {reps} pinned host arrays (public API; per step: "
+                           "H2D + kernel + D2H, consecutive steps overlapped)")
             e2e = rec
         else:
             rec["path"] = ("one blocking call per array on a pinned host tensor "

@@ -155,6 +155,21 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
                        int inverse, void* stream);
 
 /*
+ * bitrev_dit_prepass over `count` host arrays with the transfers overlapped,
+ * like bitrev_host_pipeline: array k's host->device copy runs beside array
+ * k-1's kernel and array k-2's copy back.  host_dst[k] may equal
+ * host_src[k].  Pinned host arrays overlap both copy directions; pageable
+ * ones go one array at a time through pinned bounce buffers.  Ordered after
+ * prior work on `stream`; synchronous.  dev_scratch: NULL (stream-ordered
+ * allocation) or 6 * batch * 2^b * elem_bytes bytes (an input and an output
+ * buffer for each of three slots).  No reference counterpart (SURVEY.md 8(f)
+ * f2, the batched FFT pre-pass of BASELINE config 4 on host data).
+ */
+int bitrev_dit_prepass_host_pipeline(const void* const* host_src, void* const* host_dst,
+                                     int64_t count, int b, int elem_bytes, int64_t batch,
+                                     int stages, int inverse, void* dev_scratch, void* stream);
+
+/*
  * Steps 1+2 of the top-bit sharded plan fused (no reference counterpart;
  * SURVEY.md 8(e)): rank `rank` of G = 2^g bit-reverses its local shard of
  * 2^b_local elements and stores each destination row straight into

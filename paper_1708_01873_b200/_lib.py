@@ -35,6 +35,8 @@ SIGNATURES = {
     "bitrev_swap_schedule": (_c_int, [_c_int, _vp, _vp]),
     "bitrev_dit_prepass": (_c_int, [_vp, _vp, _c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_int,
                                     _c_int, _vp]),
+    "bitrev_dit_prepass_host_pipeline": (_c_int, [_vp, _vp, _c_i64, _c_int, _c_int, _c_i64,
+                                                  _c_int, _c_int, _vp, _vp]),
     "bitrev_sharded_scatter": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "bitrev_sharded_pack": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "bitrev_sharded_unpack": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _vp]),

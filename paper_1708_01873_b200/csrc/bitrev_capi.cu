@@ -1371,42 +1371,25 @@ int bitrev_inplace_host(void* host_a, int b, int elem_bytes, int64_t batch, void
   return rc;
 }
 
-int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int64_t count, int b,
-                         int elem_bytes, int64_t batch, void* dev_scratch, void* stream) {
-  int rc = check_common(b, elem_bytes, batch);
-  if (rc) return rc;
-  if (count < 0) return BITREV_EBATCH;
-  if (count == 0) return BITREV_OK;
-  if (!host_src || !host_dst) return BITREV_ENULL;
-  for (int64_t k = 0; k < count; ++k)
-    if (!host_src[k] || !host_dst[k]) return BITREV_ENULL;
+}  // extern "C"
+
+namespace {
+
+// The pinned-memory pipeline shared by bitrev_host_pipeline (permutation in
+// place in each slot) and bitrev_dit_prepass_host_pipeline (FFT pre-pass out
+// of place: two buffers per slot): array k's H2D (sin[0..1]) overlaps array
+// k-1's kernel (sk) and array k-2's D2H (sout[0..1]), over kPipeSlots device
+// slots of `bufs` * bytes.  op(in, out, stream) runs the kernel(s) of one
+// array; out == in when bufs == 1.  Synchronous.
+template <typename Op>
+int pipeline_run(const void* const* host_src, void* const* host_dst, int64_t count, size_t bytes,
+                 int bufs, Op op, void* dev_scratch, cudaStream_t user) {
   constexpr int kSlots = kPipeSlots;
-  const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
-  const int64_t n = int64_t(1) << b;
-  cudaStream_t user = static_cast<cudaStream_t>(stream);
-  {
-    // pageable arrays cannot overlap their copies (the runtime stages them
-    // synchronously): run each through the bounce-ring single call instead
-    bool any_pageable = false;
-    for (int64_t k = 0; k < count && !any_pageable; ++k)
-      any_pageable = pageable(host_src[k]) || pageable(host_dst[k]);
-    if (any_pageable) {
-      for (int64_t k = 0; k < count; ++k) {
-        if (host_src[k] != host_dst[k]) {
-          rc = bitrev_oop_host(host_src[k], host_dst[k], b, elem_bytes, batch,
-                               dev_scratch, dev_scratch ? static_cast<char*>(dev_scratch) + bytes : nullptr,
-                               stream);
-        } else {
-          rc = bitrev_inplace_host(host_dst[k], b, elem_bytes, batch, dev_scratch, stream);
-        }
-        if (rc != BITREV_OK) return rc;
-      }
-      return BITREV_OK;
-    }
-  }
+  const size_t slot_bytes = bytes * (size_t)bufs;
   void* own = nullptr;
   char* slots = static_cast<char*>(dev_scratch);
   cudaError_t e = cudaSuccess;
+  int rc = BITREV_OK;
   PipeRes* pr = nullptr;
 #define PIPE_TRY(x)              \
   do {                           \
@@ -1418,14 +1401,15 @@ int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int
   PIPE_TRY(cudaEventRecord(pr->ev_start, user));
   for (int i = 0; i < 2; ++i) PIPE_TRY(cudaStreamWaitEvent(pr->sin[i], pr->ev_start, 0));
   if (!slots) {
-    PIPE_TRY(cudaMallocAsync(&own, kSlots * bytes, pr->sin[0]));
+    PIPE_TRY(cudaMallocAsync(&own, kSlots * slot_bytes, pr->sin[0]));
     slots = static_cast<char*>(own);
     PIPE_TRY(cudaEventRecord(pr->ev_a, pr->sin[0]));  // the allocation, for sin[1]
     PIPE_TRY(cudaStreamWaitEvent(pr->sin[1], pr->ev_a, 0));
   }
   for (int64_t k = 0; k < count; ++k) {
     const int s = (int)(k % kSlots);
-    char* buf = slots + (size_t)s * bytes;
+    char* buf = slots + (size_t)s * slot_bytes;
+    char* obuf = bufs > 1 ? buf + bytes : buf;
     auto wait_out = [&](int slot) -> cudaError_t {  // both in-streams after slot's D2H
       for (int i = 0; i < 2; ++i)
         for (int j = 0; j < 2; ++j) {
@@ -1445,11 +1429,11 @@ int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int
       PIPE_TRY(cudaEventRecord(pr->ev_in[s][i], pr->sin[i]));
       PIPE_TRY(cudaStreamWaitEvent(pr->sk, pr->ev_in[s][i], 0));
     }
-    rc = bitrev_inplace(buf, b, elem_bytes, batch, n, pr->sk);
+    rc = op(buf, obuf, pr->sk);
     if (rc != BITREV_OK) goto done;
     PIPE_TRY(cudaEventRecord(pr->ev_k[s], pr->sk));
     for (int i = 0; i < 2; ++i) PIPE_TRY(cudaStreamWaitEvent(pr->sout[i], pr->ev_k[s], 0));
-    PIPE_TRY(copy_split(host_dst[k], buf, bytes, cudaMemcpyDeviceToHost, pr->sout));
+    PIPE_TRY(copy_split(host_dst[k], obuf, bytes, cudaMemcpyDeviceToHost, pr->sout));
     for (int i = 0; i < 2; ++i) PIPE_TRY(cudaEventRecord(pr->ev_out[s][i], pr->sout[i]));
   }
   // sout[0] after every D2H (each D2H after its kernel, each kernel after its H2D)
@@ -1473,6 +1457,93 @@ done:
   if (own) cudaFree(own);  // only on an error path: the normal path frees stream-ordered
   if (rc != BITREV_OK) return rc;
   return e == cudaSuccess ? BITREV_OK : (int)e;
+}
+
+int check_pipeline_args(const void* const* host_src, void* const* host_dst, int64_t count) {
+  if (count < 0) return BITREV_EBATCH;
+  if (count == 0) return BITREV_OK;
+  if (!host_src || !host_dst) return BITREV_ENULL;
+  for (int64_t k = 0; k < count; ++k)
+    if (!host_src[k] || !host_dst[k]) return BITREV_ENULL;
+  return BITREV_OK;
+}
+
+bool any_pageable(const void* const* host_src, void* const* host_dst, int64_t count) {
+  for (int64_t k = 0; k < count; ++k)
+    if (pageable(host_src[k]) || pageable(host_dst[k])) return true;
+  return false;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bitrev_host_pipeline(const void* const* host_src, void* const* host_dst, int64_t count, int b,
+                         int elem_bytes, int64_t batch, void* dev_scratch, void* stream) {
+  int rc = check_common(b, elem_bytes, batch);
+  if (rc) return rc;
+  if ((rc = check_pipeline_args(host_src, host_dst, count)) != BITREV_OK || count == 0) return rc;
+  const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
+  const int64_t n = int64_t(1) << b;
+  if (any_pageable(host_src, host_dst, count)) {
+    // pageable arrays cannot overlap their copies (the runtime stages them
+    // synchronously): run each through the bounce-ring single call instead
+    for (int64_t k = 0; k < count; ++k) {
+      if (host_src[k] != host_dst[k]) {
+        rc = bitrev_oop_host(host_src[k], host_dst[k], b, elem_bytes, batch, dev_scratch,
+                             dev_scratch ? static_cast<char*>(dev_scratch) + bytes : nullptr,
+                             stream);
+      } else {
+        rc = bitrev_inplace_host(host_dst[k], b, elem_bytes, batch, dev_scratch, stream);
+      }
+      if (rc != BITREV_OK) return rc;
+    }
+    return BITREV_OK;
+  }
+  auto op = [&](char* in, char*, cudaStream_t st) {
+    return bitrev_inplace(in, b, elem_bytes, batch, n, st);
+  };
+  return pipeline_run(host_src, host_dst, count, bytes, 1, op, dev_scratch,
+                      static_cast<cudaStream_t>(stream));
+}
+
+int bitrev_dit_prepass_host_pipeline(const void* const* host_src, void* const* host_dst,
+                                     int64_t count, int b, int elem_bytes, int64_t batch,
+                                     int stages, int inverse, void* dev_scratch, void* stream) {
+  if (elem_bytes != 8 && elem_bytes != 16) return BITREV_EELEM;
+  int rc = check_common(b, elem_bytes, batch);
+  if (rc) return rc;
+  if (stages < 0 || stages > b) return BITREV_ESTAGES;
+  if ((rc = check_pipeline_args(host_src, host_dst, count)) != BITREV_OK || count == 0) return rc;
+  const size_t bytes = ((size_t)1 << b) * (size_t)elem_bytes * (size_t)batch;
+  const int64_t n = int64_t(1) << b;
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  auto op = [&](char* in, char* out, cudaStream_t st) {
+    return bitrev_dit_prepass(in, out, b, elem_bytes, batch, n, n, stages, inverse, st);
+  };
+  if (any_pageable(host_src, host_dst, count)) {
+    // one array at a time through the pinned bounce ring (see bitrev_oop_host)
+    void* own = nullptr;
+    char* buf = static_cast<char*>(dev_scratch);
+    cudaError_t e = cudaSuccess;
+    if (!buf) {
+      if ((e = cudaMallocAsync(&own, 2 * bytes, user)) != cudaSuccess) return (int)e;
+      buf = static_cast<char*>(own);
+    }
+    for (int64_t k = 0; k < count && rc == BITREV_OK && e == cudaSuccess; ++k) {
+      if ((e = h2d_staged(buf, host_src[k], bytes, user)) != cudaSuccess) break;
+      if ((rc = op(buf, buf + bytes, user)) != BITREV_OK) break;
+      e = d2h_staged(host_dst[k], buf + bytes, bytes, user);
+    }
+    if (own) {
+      const cudaError_t f = cudaFreeAsync(own, user);
+      const cudaError_t s2 = cudaStreamSynchronize(user);
+      if (e == cudaSuccess) e = f != cudaSuccess ? f : s2;
+    }
+    if (rc != BITREV_OK) return rc;
+    return e == cudaSuccess ? BITREV_OK : (int)e;
+  }
+  return pipeline_run(host_src, host_dst, count, bytes, 2, op, dev_scratch, user);
 }
 
 int bitrev_transpose_square(void* a, int h, int elem_bytes, int64_t batch, int64_t batch_stride,

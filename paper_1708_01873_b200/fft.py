@@ -11,6 +11,8 @@ complete (unnormalised) radix-2 FFT.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _core, _lib
@@ -61,6 +63,56 @@ def bitrev_dit_prepass(x, b: int, stages: int, inverse: bool = False, out=None) 
     if dst_d is not dst:
         dst.copy_(dst_d)
     return dst
+
+
+def dit_prepass_host_pipeline(arrays, b: int, stages: int, out=None,
+                              inverse: bool = False) -> list:
+    """bitrev_dit_prepass over many host arrays with overlapped transfers.
+
+    arrays: host arrays (torch CPU tensors or numpy arrays) of one shape
+    ([2^b] or [batch, 2^b]) and complex dtype, contiguous.  out: matching
+    destination host arrays, or None to write each result over its input.
+    Array k's host->device copy overlaps array k-1's kernel and array k-2's
+    device->host copy (bitrev_dit_prepass_host_pipeline in the C ABI); pinned
+    host memory lets both copy directions run at once.  Synchronous; returns
+    the destination list.
+    """
+    srcs = [as_tensor(a, "arrays[k]") for a in arrays]
+    if not srcs:
+        return []
+    first = srcs[0]
+    if first.dtype not in _COMPLEX:
+        raise ValueError(f"dtype {first.dtype} is not complex64/complex128")
+    check_width(b)
+    if first.dim() not in (1, 2) or first.shape[-1] != (1 << b):
+        raise ValueError(f"arrays[k] length {first.shape[-1]} does not match 2**{b}")
+    if not 0 <= stages <= b:
+        raise ValueError(f"stages must be in 0..{b}, got {stages}")
+    for t in srcs:
+        if t.is_cuda:
+            raise ValueError("dit_prepass_host_pipeline takes host arrays; use "
+                             "bitrev_dit_prepass for CUDA tensors")
+        if t.shape != first.shape or t.dtype != first.dtype:
+            raise ValueError("all arrays must share shape and dtype")
+        if not t.is_contiguous():
+            raise ValueError("arrays must be contiguous")
+    dsts = srcs if out is None else [as_tensor(o, "out[k]") for o in out]
+    if len(dsts) != len(srcs):
+        raise ValueError("out must have one destination per array")
+    for d in dsts:
+        if d.is_cuda or d.shape != first.shape or d.dtype != first.dtype or not d.is_contiguous():
+            raise ValueError("out arrays must be contiguous host arrays shaped like the inputs")
+    dev = _core.require_cuda()
+    n = len(srcs)
+    batch = 1 if first.dim() == 1 else first.shape[0]
+    src_ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in srcs])
+    dst_ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in dsts])
+    scratch = torch.empty(6 * first.numel() * first.element_size(), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("bitrev_dit_prepass_host_pipeline", ctypes.cast(src_ptrs, ctypes.c_void_p),
+                  ctypes.cast(dst_ptrs, ctypes.c_void_p), n, b, _COMPLEX[first.dtype], batch,
+                  stages, int(bool(inverse)), scratch.data_ptr(), _core._stream_ptr(dev))
+    return list(out) if out is not None else list(arrays)
 
 
 def max_fused_stages(b: int, elem_bytes: int) -> int:

@@ -137,3 +137,45 @@ def test_wide_rows_tier_complex64(cuda, b, rows, stages):
         got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages, inverse=inverse)
         ref = np.stack([dit_reference(r, b, stages, inverse) for r in x])
         check(got, ref, torch.complex64, stages)
+
+
+@pytest.mark.parametrize("stages,pinned", [(7, True), (3, True), (5, False)])
+def test_dit_prepass_host_pipeline(cuda, stages, pinned):
+    """dit_prepass_host_pipeline over host arrays (pinned: overlapped copies;
+    numpy/pageable: the bounce-ring path), out of place and over the inputs,
+    a recurring array included: every result equals the device call's bytes."""
+    b, rows = 16, 24
+    xs = [rand_complex((rows, 1 << b), torch.complex64, 90 + k) for k in range(4)]
+    want = [br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages).cpu() for x in xs]
+    if pinned:
+        hs = [torch.from_numpy(x).pin_memory() for x in xs]
+        outs = [torch.empty_like(h).pin_memory() for h in hs]
+    else:
+        hs = [x.copy() for x in xs]
+        outs = [np.empty_like(x) for x in xs]
+    seq_in = hs + [hs[0]]
+    seq_out = outs + [outs[0]]
+    got = br.dit_prepass_host_pipeline(seq_in, b, stages, out=seq_out)
+    for k in range(4):
+        g = torch.as_tensor(got[k])
+        assert torch.equal(g.view(torch.uint8), want[k].view(torch.uint8)), k
+    # in place on the host (out=None): each input replaced by its result
+    ins = [h.clone() if pinned else h.copy() for h in hs]
+    if pinned:
+        ins = [t.pin_memory() for t in ins]
+    br.dit_prepass_host_pipeline(ins, b, stages)
+    for k in range(4):
+        assert torch.equal(torch.as_tensor(ins[k]).view(torch.uint8), want[k].view(torch.uint8))
+
+
+def test_dit_prepass_host_pipeline_validation(cuda):
+    x = torch.zeros(1 << 10, dtype=torch.complex64)
+    with pytest.raises(ValueError, match="complex"):
+        br.dit_prepass_host_pipeline([torch.zeros(1 << 10)], 10, 2)
+    with pytest.raises(ValueError, match="stages"):
+        br.dit_prepass_host_pipeline([x], 10, 11)
+    with pytest.raises(ValueError, match="host arrays"):
+        br.dit_prepass_host_pipeline([x.to(cuda)], 10, 2)
+    with pytest.raises(ValueError, match="one destination"):
+        br.dit_prepass_host_pipeline([x, x.clone()], 10, 2, out=[x.clone()])
+    assert br.dit_prepass_host_pipeline([], 10, 2) == []
