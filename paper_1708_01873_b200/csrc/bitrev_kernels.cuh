@@ -1724,6 +1724,82 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
   }
 }
 
+// complex128, 1..STAGES (<= 5; the host uses it for 1-3) fused stages on the square Q6 tiles of the
+// out-of-place complex128 kernel (1 KB rows on both sides, cfg3-16's shape).
+// A drain item is one 16-byte element: with 256 threads and 64 elements per
+// destination row, a thread's column x = tid % 64 is the same for every item
+// it drains, and a warp holds 32 consecutive x of one row.  Stage s pairs x
+// with x ^ 2^(s-1) -- lane ^ 2^(s-1) for s <= 5 -- so the butterflies run
+// on warp shuffles of the four 32-bit words, with twiddles W_{2^s}^(x mod
+// 2^(s-1)) fixed per thread (computed once).
+template <int STAGES, bool CS = false>
+__global__ void __launch_bounds__(256, 1) bitrev_fft_tile16_kernel(FftArgs fa) {
+  static_assert(STAGES >= 1 && STAGES <= 5, "shuffle stages stay inside a warp");
+  using T = Tile<16, 6, 256>;
+  extern __shared__ __align__(16) uint4 smem[];
+  const TileArgs& a = fa.t;
+  const uint64_t row_stride = (uint64_t)16 << (a.b - 6);
+  const uint64_t mmask = (1ull << a.m) - 1;
+  uint4 r[T::IPT][T::V];
+  const int x = threadIdx.x & 63, lane = threadIdx.x & 31;
+  double2 tw[STAGES + 1];  // tw[s] = W_{2^s}^(x mod 2^(s-1))
+#pragma unroll
+  for (int s = 1; s <= STAGES; ++s) {
+    const int k = x & ((1 << (s - 1)) - 1);
+    double sn, cs;
+    sincospi((fa.inverse ? 2.0 : -2.0) * k / (1 << s), &sn, &cs);
+    tw[s] = make_double2(cs, sn);
+  }
+  auto dv = [](const uint4& u) {
+    return make_double2(__hiloint2double((int)u.y, (int)u.x), __hiloint2double((int)u.w, (int)u.z));
+  };
+  auto ud = [](const double2& d) {
+    return make_uint4((unsigned)__double2loint(d.x), (unsigned)__double2hiint(d.x),
+                      (unsigned)__double2loint(d.y), (unsigned)__double2hiint(d.y));
+  };
+
+  uint64_t t = blockIdx.x;
+  if (t >= a.ntiles) return;
+  auto src_tile = [&](uint64_t tt) {
+    const uint64_t bi = tt >> a.m, y = tt & mmask;
+    return a.src + bi * a.src_bstride + (y << 6) * 16;
+  };
+  tile_load<16, 6, true, 256, CS && BITREV_LD_CS>(r, src_tile(t), row_stride);
+  for (;;) {
+    const uint64_t bi = t >> a.m, y = t & mmask;
+    tile_stage<16, 6, 256>(r, smem);
+    __syncthreads();
+    const uint64_t tn = t + gridDim.x;
+    if (tn < a.ntiles) tile_load<16, 6, true, 256, CS && BITREV_LD_CS>(r, src_tile(tn), row_stride);
+    char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << 6) * 16;
+#pragma unroll
+    for (int it = 0; it < T::WPT; ++it) {
+      const int id = it * 256 + threadIdx.x;
+      const int z = id >> 6;  // column id & 63 == x
+      double2 v = dv(smem[swz<16, 6>(z, x)]);
+#pragma unroll
+      for (int s = 1; s <= STAGES; ++s) {
+        const int h = 1 << (s - 1);
+        double2 p;
+        p.x = __shfl_xor_sync(0xffffffffu, v.x, h);
+        p.y = __shfl_xor_sync(0xffffffffu, v.y, h);
+        const bool upper = lane & h;
+        const double2 b = upper ? v : p;  // the pair's odd element
+        const double2 w = tw[s];
+        const double2 wb = make_double2(b.x * w.x - b.y * w.y, b.x * w.y + b.y * w.x);
+        const double2 top = upper ? p : v;
+        v = upper ? make_double2(top.x - wb.x, top.y - wb.y)
+                  : make_double2(top.x + wb.x, top.y + wb.y);
+      }
+      const uint64_t rz = __brev((unsigned)z) >> (32 - 6);
+      st_vec<CS>(dbase + rz * row_stride + (uint64_t)x * 16, ud(v));
+    }
+    if (tn >= a.ntiles) break;
+    __syncthreads();
+    t = tn;
+  }
+}
+
 // Rectangular-tile FFT pre-pass (bitrev_oop_rect_kernel's load/stage path).
 template <int E, int QX, int QZ, int STAGES>
 __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
