@@ -1744,15 +1744,20 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     }
     return finish_launch();
   }
-  // complex128 with 1-3 stages: the square Q6 tiles of the out-of-place
+  // complex128 with 1-5 stages: the square Q6 tiles of the out-of-place
   // kernel (1 KB rows on both sides) with the stages on warp shuffles in the
-  // drain (bitrev_fft_tile16_kernel): 2048 x 2^16, 1 / 2 / 3 stages 5986 /
-  // 5701 / 6402 -> 6464 / 6400 / 6698 GB/s; at 4 / 5 stages the FP64 +
-  // shuffle work loses 15 / 30 % to the radix-4 drain below
-  // (tools/fft_c128_tile_ab.sh -> profiles/r02_fft_c128_tile_ab.txt).
-  // BITREV_B200_FFT_C128_TILE=0 keeps the rectangular tiles (A/B runs).
+  // drain (bitrev_fft_tile16_kernel, select-free butterflies): 2048 x 2^16,
+  // 1 / 2 / 3 / 4 / 5 stages 5988 / 5698 / 6401 / 6330 / 5987 ->
+  // 6494 / 6425 / 6405 / 6758 / 6100 GB/s against the rectangular radix-4
+  // drain (tools/fft_c128_tile_ab.sh, fft_c128_tile2_ab.sh ->
+  // profiles/r02_fft_c128_tile*_ab.txt; the first form, with selects, lost
+  // 15 / 30 % at 4 / 5 stages).  BITREV_B200_FFT_C128_TILE=0 keeps the
+  // rectangular tiles, BITREV_B200_FFT_C128_TILE_MAX caps the stage count
+  // (A/B runs).
   static const int c128_tile = env_int("BITREV_B200_FFT_C128_TILE", 1);
-  if (E == 16 && c128_tile && stages <= 3 && b >= 12 && aligned16(src) && aligned16(dst)) {
+  static const int c128_tile_max = env_int("BITREV_B200_FFT_C128_TILE_MAX", 5);
+  if (E == 16 && c128_tile && stages <= c128_tile_max && b >= 12 && aligned16(src) &&
+      aligned16(dst)) {
     a.m = b - 12;
     a.ntiles = (uint64_t)batch << a.m;
     constexpr int kBytes = 64 * 64 * 16;
@@ -1764,7 +1769,7 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     kern<<<grid_for(a.ntiles, per_sm), 256, kBytes, st>>>(fa);                           \
     return finish_launch();                                                              \
   }
-    switch (stages) { FFT16_LAUNCH(1) FFT16_LAUNCH(2) FFT16_LAUNCH(3) }
+    switch (stages) { FFT16_LAUNCH(1) FFT16_LAUNCH(2) FFT16_LAUNCH(3) FFT16_LAUNCH(4) FFT16_LAUNCH(5) }
 #undef FFT16_LAUNCH
   }
   // Fused path: rectangular tiles whose destination rows are the FFT blocks

@@ -1724,7 +1724,7 @@ __device__ __forceinline__ void fft_rows_drain_r8(uint4* U, char* dbase, uint64_
   }
 }
 
-// complex128, 1..STAGES (<= 5; the host uses it for 1-3) fused stages on the square Q6 tiles of the
+// complex128, 1..STAGES (<= 5) fused stages on the square Q6 tiles of the
 // out-of-place complex128 kernel (1 KB rows on both sides, cfg3-16's shape).
 // A drain item is one 16-byte element: with 256 threads and 64 elements per
 // destination row, a thread's column x = tid % 64 is the same for every item
@@ -1741,14 +1741,22 @@ __global__ void __launch_bounds__(256, 1) bitrev_fft_tile16_kernel(FftArgs fa) {
   const uint64_t row_stride = (uint64_t)16 << (a.b - 6);
   const uint64_t mmask = (1ull << a.m) - 1;
   uint4 r[T::IPT][T::V];
-  const int x = threadIdx.x & 63, lane = threadIdx.x & 31;
-  double2 tw[STAGES + 1];  // tw[s] = W_{2^s}^(x mod 2^(s-1))
+  const int x = threadIdx.x & 63;
+  // Stage s, pair (x, x + h), h = 2^(s-1): the lower lane needs v + w p, the
+  // upper one p - w v.  Each lane first scales its own value by wp[s] (w in
+  // the upper lane, 1 in the lower), swaps the scaled values with its
+  // partner, and adds: out = other + sgn[s] * own (sgn = -1 in the upper
+  // lane) -- no selects.  w = W_{2^s}^(x mod h); stage 1 has w = 1.
+  double2 wp[STAGES + 1];
+  double sgn[STAGES + 1];
 #pragma unroll
   for (int s = 1; s <= STAGES; ++s) {
-    const int k = x & ((1 << (s - 1)) - 1);
-    double sn, cs;
-    sincospi((fa.inverse ? 2.0 : -2.0) * k / (1 << s), &sn, &cs);
-    tw[s] = make_double2(cs, sn);
+    const int h = 1 << (s - 1);
+    const bool upper = x & h;
+    double sn = 0.0, cs = 1.0;
+    if (upper) sincospi((fa.inverse ? 2.0 : -2.0) * (x & (h - 1)) / (1 << s), &sn, &cs);
+    wp[s] = make_double2(cs, sn);
+    sgn[s] = upper ? -1.0 : 1.0;
   }
   auto dv = [](const uint4& u) {
     return make_double2(__hiloint2double((int)u.y, (int)u.x), __hiloint2double((int)u.w, (int)u.z));
@@ -1780,16 +1788,15 @@ __global__ void __launch_bounds__(256, 1) bitrev_fft_tile16_kernel(FftArgs fa) {
 #pragma unroll
       for (int s = 1; s <= STAGES; ++s) {
         const int h = 1 << (s - 1);
-        double2 p;
-        p.x = __shfl_xor_sync(0xffffffffu, v.x, h);
-        p.y = __shfl_xor_sync(0xffffffffu, v.y, h);
-        const bool upper = lane & h;
-        const double2 b = upper ? v : p;  // the pair's odd element
-        const double2 w = tw[s];
-        const double2 wb = make_double2(b.x * w.x - b.y * w.y, b.x * w.y + b.y * w.x);
-        const double2 top = upper ? p : v;
-        v = upper ? make_double2(top.x - wb.x, top.y - wb.y)
-                  : make_double2(top.x + wb.x, top.y + wb.y);
+        double2 e = v;
+        if (s > 1) {
+          const double2 w = wp[s];
+          e = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+        }
+        double2 o;
+        o.x = __shfl_xor_sync(0xffffffffu, e.x, h);
+        o.y = __shfl_xor_sync(0xffffffffu, e.y, h);
+        v = make_double2(fma(sgn[s], e.x, o.x), fma(sgn[s], e.y, o.y));
       }
       const uint64_t rz = __brev((unsigned)z) >> (32 - 6);
       st_vec<CS>(dbase + rz * row_stride + (uint64_t)x * 16, ud(v));

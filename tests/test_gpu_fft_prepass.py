@@ -184,10 +184,9 @@ def test_dit_prepass_host_pipeline_validation(cuda):
 @pytest.mark.parametrize("b,rows", [(12, 16), (14, 4), (18, 1)])
 @pytest.mark.parametrize("stages", [1, 2, 3, 4, 5])
 def test_complex128_square_tiles_shuffle_stages(cuda, b, rows, stages):
-    """complex128 with 1-5 stages on rows of 2^12 and up (1-3: the square Q6 tiles
-    with the butterflies on warp shuffles, bitrev_fft_tile16_kernel; 4-5: the
-    rectangular tiles), forward and inverse, every row against the float64
-    restatement."""
+    """complex128 with 1-5 stages on rows of 2^12 and up: the square Q6 tiles
+    with the butterflies on warp shuffles (bitrev_fft_tile16_kernel), forward
+    and inverse, every row against the float64 restatement."""
     x = rand_complex((rows, 1 << b), torch.complex128, 200 + 10 * b + stages)
     for inverse in (False, True):
         got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages, inverse=inverse)
