@@ -192,3 +192,30 @@ def test_complex128_square_tiles_shuffle_stages(cuda, b, rows, stages):
         got = br.bitrev_dit_prepass(torch.from_numpy(x).to(cuda), b, stages, inverse=inverse)
         ref = np.stack([dit_reference(r, b, stages, inverse) for r in x])
         check(got, ref, torch.complex128, stages)
+
+
+@pytest.mark.parametrize("dtype,b,rows,stages", [
+    (torch.complex64, 16, 80, 3),    # 256-element rows (>= 16 MiB)
+    (torch.complex64, 16, 8, 7),     # 128-element rows, radix-8 drain
+    (torch.complex128, 14, 8, 2),    # square tiles, shuffle stages
+    (torch.complex128, 14, 8, 6),    # rectangular tiles, radix-4 drain
+])
+def test_strided_rows_through_the_c_abi(cuda, dtype, b, rows, stages):
+    """bitrev_dit_prepass with batch strides wider than the rows (rows inside
+    padded buffers): results equal the contiguous call's bytes and the pads
+    on both sides stay untouched."""
+    from paper_1708_01873_b200 import _core, _lib
+
+    n, sp, dp = 1 << b, 24, 40
+    E = 8 if dtype == torch.complex64 else 16
+    x = torch.from_numpy(rand_complex((rows, n), dtype, 300 + b + stages)).to(cuda)
+    src = torch.full((rows, n + sp), complex(7.0, -7.0), dtype=dtype, device=cuda)
+    src[:, :n] = x
+    dst = torch.full((rows, n + dp), complex(3.0, 5.0), dtype=dtype, device=cuda)
+    _lib.call("bitrev_dit_prepass", src.data_ptr(), dst.data_ptr(), b, E, rows, n + sp, n + dp,
+              stages, 0, _core._stream_ptr(x.device))
+    want = br.bitrev_dit_prepass(x, b, stages)
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:, :n].view(torch.uint8), want.view(torch.uint8))
+    assert bool((dst[:, n:] == complex(3.0, 5.0)).all())
+    assert bool((src[:, n:] == complex(7.0, -7.0)).all())
