@@ -1905,7 +1905,15 @@ int bitrev_sharded_unpack(const void* recv, void* dst, int b_local, int g, int e
                    (E == 4 || E == 8 || E == 16);
   if (vec) {
     const uint64_t threads = C / (16 / E);
-    const unsigned grid = (unsigned)grid_for((threads + 255) / 256, 8);
+    // A grid of up to 256 CTAs per SM (2-4 resident by registers, the rest
+    // queued; each CTA strides over few blocks) against 8 per SM: G = 2 / 4 /
+    // 8 at the cfg5 shard sizes 6357 / 6132 / 6245 -> 6446 / 6650 / 6688 GB/s
+    // (tools/unpack_grid_ab.py -> profiles/r02_unpack_grid_ab*.jsonl).  Short
+    // grid-stride loops also let CTAs retire throughout the kernel, which
+    // frees SM slots for NCCL's CTAs while later rounds are on the wire.
+    // BITREV_B200_UNPACK_PER_SM overrides it (A/B runs).
+    static const int per_sm = env_int("BITREV_B200_UNPACK_PER_SM", 256);
+    const unsigned grid = (unsigned)grid_for((threads + 255) / 256, per_sm > 0 ? per_sm : 256);
 #define UNPACK_G(E_, G_)                                                  \
   case G_:                                                                \
     sharded_unpack_kernel<E_, G_><<<grid, 256, 0, st>>>(r, d, C);         \
