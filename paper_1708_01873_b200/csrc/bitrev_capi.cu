@@ -224,6 +224,29 @@ int prepare_kernel(K kernel, int threads, int smem_bytes) {
 // ---------------------------------------------------------------------------
 // tile launches
 
+// Out-of-place tile grids: not one persistent CTA per SM slot but about
+// kOopTilesPerCta tiles per CTA, so the resident CTAs start on tiles far
+// apart and the block scheduler keeps refilling SMs with new CTAs.  Each CTA
+// still prefetches its next tile into registers.  cfg3-16 6529 -> 6712
+// GB/s (~7 tiles per CTA), cfg3-8 6320 -> 6677 (~3.5), cfg4 6370 -> 6545
+// (~3.5), cfg5 on one GPU 6308 -> 6610 (~7); float32 (the 1-CTA/SM (8,6)
+// tiles) and the in-place pairs lose, so they stay persistent
+// (tools/grid_mult_sweep.sh -> profiles/r02_grid_mult_sweep.jsonl).  Only
+// launches with at least 16 such grids' worth of waves take it: at 1.4-5.5
+// waves the last wave's idle SMs cost up to 15 % (complex128 at 64 MiB,
+// float64 at 32-64 MiB; tools/oop_tpc_ab.sh -> profiles/r02_oop_tpc_ab.jsonl).
+// BITREV_B200_OOP_TILES_PER_CTA overrides the target (0 = persistent).
+int oop_grid(int E, uint64_t ntiles, int per_sm) {
+  const int resident = grid_for(ntiles, per_sm);
+  static const int env = env_int("BITREV_B200_OOP_TILES_PER_CTA", -1);
+  const int tpc = env >= 0 ? env : (E == 4 ? 0 : 5);
+  if (tpc <= 0) return resident;
+  const uint64_t want = ntiles / (uint64_t)tpc;
+  if (want < 16ull * (uint64_t)resident) return resident;
+  return (int)(want < (1ull << 31) - 1 ? want : (1ull << 31) - 1);
+}
+
+
 template <int E, int Q, int NT = BITREV_TILE_THREADS>
 int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sbs, int64_t dbs,
                     cudaStream_t st) {
@@ -253,7 +276,7 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
   a.order = tile_order(false);
   a.npairs = 0;
   a.batch = batch;
-  const int grid = grid_for(a.ntiles, per_sm);
+  const int grid = oop_grid(E, a.ntiles, per_sm);
   kern<<<grid, T::THREADS, T::BYTES, st>>>(a);
   return finish_launch();
 }
@@ -533,7 +556,7 @@ int launch_oop_rect(const void* src, void* dst, int b, int64_t batch, int64_t sb
   a.order = tile_order(false);
   a.npairs = 0;
   a.batch = batch;
-  const int grid = grid_for(a.ntiles, per_sm);
+  const int grid = oop_grid(E, a.ntiles, per_sm);
   kern<<<grid, T::THREADS, smem, st>>>(a);
   return finish_launch();
 }
