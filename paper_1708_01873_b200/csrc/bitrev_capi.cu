@@ -236,14 +236,33 @@ int prepare_kernel(K kernel, int threads, int smem_bytes) {
 // waves the last wave's idle SMs cost up to 15 % (complex128 at 64 MiB,
 // float64 at 32-64 MiB; tools/oop_tpc_ab.sh -> profiles/r02_oop_tpc_ab.jsonl).
 // BITREV_B200_OOP_TILES_PER_CTA overrides the target (0 = persistent).
-int oop_grid(int E, uint64_t ntiles, int per_sm) {
+int spread_grid(uint64_t ntiles, int per_sm, int tpc) {
   const int resident = grid_for(ntiles, per_sm);
-  static const int env = env_int("BITREV_B200_OOP_TILES_PER_CTA", -1);
-  const int tpc = env >= 0 ? env : (E == 4 ? 0 : 5);
   if (tpc <= 0) return resident;
   const uint64_t want = ntiles / (uint64_t)tpc;
   if (want < 16ull * (uint64_t)resident) return resident;
   return (int)(want < (1ull << 31) - 1 ? want : (1ull << 31) - 1);
+}
+
+int oop_grid(int E, uint64_t ntiles, int per_sm) {
+  static const int env = env_int("BITREV_B200_OOP_TILES_PER_CTA", -1);
+  return spread_grid(ntiles, per_sm, env >= 0 ? env : (E == 4 ? 0 : 5));
+}
+
+// The same for the sharded pack / fused scatter and the FFT pre-pass tiles
+// (tools/spread_grid_ab.sh -> profiles/r02_spread_grid_ab.*): the pack and
+// scatter move by -1 to +0.6 %, so they stay persistent; the complex128
+// square-tile FFT takes it at 1-3 stages (+2 to +6.5 %; -14 % at 4-5), the
+// complex64 FFT tiles keep persistent grids (-1 to -8 % at 1-5 stages,
+// within 1.5 % at 6-7).  BITREV_B200_PACK_TILES_PER_CTA /
+// BITREV_B200_FFT_TILES_PER_CTA override (A/B runs).
+int pack_grid(uint64_t ntiles, int per_sm) {
+  static const int env = env_int("BITREV_B200_PACK_TILES_PER_CTA", 0);
+  return spread_grid(ntiles, per_sm, env);
+}
+int fft_grid(uint64_t ntiles, int per_sm, int dflt = 0) {
+  static const int env = env_int("BITREV_B200_FFT_TILES_PER_CTA", -1);
+  return spread_grid(ntiles, per_sm, env >= 0 ? env : dflt);
 }
 
 
@@ -1188,7 +1207,7 @@ int launch_pack_rect(const void* src, char* const* peer, int rank, int b, int g,
   pa.g = g;
   pa.sb = sb;
   pa.rank = rank;
-  kern<<<grid_for(a.ntiles, per_sm), T::THREADS, smem, st>>>(pa);
+  kern<<<pack_grid(a.ntiles, per_sm), T::THREADS, smem, st>>>(pa);
   return finish_launch();
 }
 
@@ -1789,7 +1808,7 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     auto kern = stream_stores(16, b, batch) ? bitrev_fft_tile16_kernel<S_, true>         \
                                             : bitrev_fft_tile16_kernel<S_, false>;       \
     const int per_sm = prepare_kernel(kern, 256, kBytes);                                \
-    kern<<<grid_for(a.ntiles, per_sm), 256, kBytes, st>>>(fa);                           \
+    kern<<<fft_grid(a.ntiles, per_sm, S_ <= 3 ? 5 : 0), 256, kBytes, st>>>(fa);          \
     return finish_launch();                                                              \
   }
     switch (stages) { FFT16_LAUNCH(1) FFT16_LAUNCH(2) FFT16_LAUNCH(3) FFT16_LAUNCH(4) FFT16_LAUNCH(5) }
@@ -1840,7 +1859,7 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     using T = Rect<E_, QX_, QZ_>;                                                            \
     auto kern = bitrev_fft_rect_kernel<E_, QX_, QZ_, S_>;                                    \
     const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);                           \
-    kern<<<grid_for(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                      \
+    kern<<<fft_grid(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                       \
     return finish_launch();                                                                  \
   }
   if (wide && qz == 5) {
