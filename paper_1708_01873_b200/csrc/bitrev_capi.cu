@@ -699,7 +699,13 @@ int launch_rows(const void* src, void* dst, int b, int64_t batch, int64_t sbs, i
   const bool ip = src == dst;
   auto kern = ip ? bitrev_rows_kernel<E, true, KB> : bitrev_rows_kernel<E, false, KB>;
   const int per_sm = prepare_kernel(kern, R::THREADS, R::BYTES);
-  const int grid = grid_for((uint64_t)nblocks, per_sm);
+  // ~2 blocks per CTA instead of a persistent grid (see oop_grid) for 8- and
+  // 16-byte rows: batches of 2^26 elements as rows of 2^6..2^12, in and out
+  // of place, 6.0-6.4 -> 6.6-6.9 TB/s; float32 rows unchanged
+  // (tools/small_rows_probe.py -> profiles/r02_rows_tpc_ab.jsonl).
+  // BITREV_B200_ROWS_TILES_PER_CTA overrides it (A/B runs).
+  static const int rows_env = env_int("BITREV_B200_ROWS_TILES_PER_CTA", -1);
+  const int grid = spread_grid((uint64_t)nblocks, per_sm, rows_env >= 0 ? rows_env : (E == 4 ? 0 : 2));
   kern<<<grid, R::THREADS, R::BYTES, st>>>(static_cast<const char*>(src), static_cast<char*>(dst),
                                             b, batch, sbs * E, dbs * E, sh);
   return finish_launch();
