@@ -604,7 +604,10 @@ def e2e_host(torch, br, x, b, E, inplace, workload, steps, stream):
     hosts = [x.cpu().pin_memory() for _ in range(nhost)]
     houts = None if inplace else [torch.empty_like(h).pin_memory() for h in hosts]
     cfg = br.CobraConfig(6)
-    reps = max(3, min(steps, 32))
+    # arrays streamed through the pipeline: its first H2D and last D2H have
+    # no opposite-direction copy to overlap, so the per-step figure
+    # approaches the steady state as 1 - ~1/reps (48: within ~2 %)
+    reps = min(64, max(48, steps))
     e2e = e2e_single = None
 
     def run_pipeline():
