@@ -1830,12 +1830,12 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
   // (16 rows: +29 % at 4 stages); complex64 with QZ = 5 needs ~170 registers
   // (1 CTA/SM) and trails QZ = 4 once the drain's shared-memory conflicts are
   // gone.
-  // complex64: 256-byte source pieces (QZ = 5, 32 KB tiles, 2 CTAs/SM) for 2-6
-  // fused stages, 128-byte pieces (QZ = 4, 3 CTAs/SM) for 1 and 7: measured
-  // A/B (profiles/r02_fft_qz_ab.txt): QZ = 5 +1 % / +3 % / +3 % / +5 % / +7 %
-  // at 2 / 3 / 4 / 5 / 6 stages, -0.4 % at 1 stage, -2 % at 7 (the third
-  // layout exchange tips it into issue-bound).  BITREV_B200_FFT_QZ=4|5 forces
-  // one shape (A/B runs).
+  // complex64: 256-byte source pieces (QZ = 5, 32 KB tiles, 2 CTAs/SM) for 2-7
+  // fused stages, 128-byte pieces (QZ = 4, 3 CTAs/SM) for 1: measured A/B
+  // (profiles/r02_fft_qz_ab.txt): QZ = 5 +1 % / +3 % / +3 % / +5 % / +7 % at
+  // 2 / 3 / 4 / 5 / 6 stages, -0.4 % at 1 stage; with the radix-8 drain also
+  // +2-4 % at 7 (cfg4-fft7 5646 vs 5493-5564 GB/s, same box).
+  // BITREV_B200_FFT_QZ=4|5 forces one shape (A/B runs).
   static const int qz_env = env_int("BITREV_B200_FFT_QZ", 0);
   // complex64: 256-element destination rows (QX = 8: two 128-element FFT
   // blocks per row, radix-8 drain, 64 KB tiles at 1 CTA/SM) against 128-element
