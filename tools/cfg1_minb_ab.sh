@@ -1,3 +1,4 @@
+# cfg1 (2^20 complex128): the Q5 tier's tile kernel at 1 / 3 / 4 CTAs/SM (BITREV_B200_SMALL_MINB), flushed and L2-hot.
 O=gpurun_out
 : > $O/cfg1_minb_ab.jsonl
 for r in 1 2 3; do

@@ -1,3 +1,4 @@
+"""In-place register pairs against the element-granular cp.async pairs (path 4) at b = 26 / 30 through tune_tiles. Measurement tool."""
 import json, os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))

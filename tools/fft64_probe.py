@@ -1,3 +1,4 @@
+"""FFT pre-pass on rows of 64 KB (complex64 2^13, complex128 2^12): tiles vs the staged-row kernel by stage count. Measurement tool."""
 import json, sys, torch
 sys.path.insert(0, '/root/repo')
 from paper_1708_01873_b200 import _lib

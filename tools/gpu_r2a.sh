@@ -1,3 +1,4 @@
+# Round-2 evidence batch: smoke, baseline-size parity tests, default bench, reference arm, cfg2 line.
 set -u
 O=gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke=$?

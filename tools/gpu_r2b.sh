@@ -1,3 +1,4 @@
+# Round-2 batch: benchmark-API tests, DRAM run-length probe, cfg5 local phases, cfg5 on one GPU.
 set -u
 O=gpurun_out
 timeout 900 python -m pytest tests/test_gpu_bench_api.py -m gpu -q -x > $O/pytest_api.log 2>&1; echo pytest=$?; tail -3 $O/pytest_api.log

@@ -1,3 +1,4 @@
+# Round-2 batch: pack/unpack parity, cfg5 phases, cfg2 lines around the tile-swap and run-length probes.
 set -u
 O=gpurun_out
 timeout 900 python -m pytest tests/test_gpu_baseline_sizes.py -m gpu -q -x -k "unpack or pack or cfg5" > $O/pytest_pack.log 2>&1; echo pytest=$?; tail -2 $O/pytest_pack.log

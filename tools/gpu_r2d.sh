@@ -1,3 +1,4 @@
+# Round-2 batch: sharded parity, cfg5 phases, run-length probe, cfg2 line.
 set -u
 O=gpurun_out
 timeout 900 python -m pytest tests/test_gpu_baseline_sizes.py tests/test_gpu_golden.py -m gpu -q -x -k "unpack or pack or cfg5 or sharded" > $O/pytest_pack2.log 2>&1; echo pytest=$?; tail -2 $O/pytest_pack2.log

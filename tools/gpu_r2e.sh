@@ -1,3 +1,4 @@
+# Round-2 batch: ncu captures of the cfg5 pack/unpack, cfg2 and cfg3-16, and the default launch list.
 set -u
 O=gpurun_out
 python tools/ncu_cfg5.py > $O/ncu_cfg5_plain.log 2>&1 && \

@@ -1,3 +1,4 @@
+# Round-2 batch: FFT stage-7 warp-shuffle variant (variants/lib_s7d.so) against the shared-memory exchange.
 set -u
 O=gpurun_out
 BITREV_B200_FFT_QZ=5 timeout 600 python -m pytest tests/test_gpu_fft_prepass.py -m gpu -q -x > $O/pytest_fft_s7.log 2>&1; echo pytest_qz5=$?; tail -1 $O/pytest_fft_s7.log

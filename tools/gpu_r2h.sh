@@ -1,3 +1,4 @@
+# Round-2 batch: radix-8 against radix-4 drain at 7 stages (variants/lib_r4.so), cfg4-fft7 line.
 set -u
 O=gpurun_out
 timeout 600 python -m pytest tests/test_gpu_fft_prepass.py -m gpu -q -x > $O/pytest_fft_r8.log 2>&1; echo pytest=$?; tail -1 $O/pytest_fft_r8.log

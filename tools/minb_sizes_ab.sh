@@ -1,3 +1,4 @@
+# complex128 Q5 tier at 1 vs 4 CTAs/SM over b = 17..21 (size curve), then the pack shared-memory A/B.
 O=gpurun_out
 : > $O/minb_sizes_ab.jsonl
 for r in 1 2; do

@@ -1,3 +1,4 @@
+"""float64 out of place, rectangular tiles at QX = 5 / 6 / 7 (b = 26 / 28 / 30), 20 back-to-back launches. Measurement tool."""
 import sys, json, torch
 sys.path.insert(0, '/root/repo')
 from paper_1708_01873_b200 import _core, _lib
