@@ -33,8 +33,8 @@ __device__ __forceinline__ void stg(void* p, const uint4& v) {
 
 // CTA of NT threads per pair; each thread moves VPT vectors of each tile.
 template <int R, int ROWS, int NT>
-__global__ void __launch_bounds__(NT) tile_swap(char* a, const uint32_t* ys, int npairs, int m,
-                                               uint64_t stride) {
+__global__ void __launch_bounds__(NT) tile_swap(char* a, char* out, const uint32_t* ys, int npairs,
+                                               int m, uint64_t stride) {
   constexpr int CPR = R / 16;                 // 16-byte chunks per row
   constexpr int VPT = ROWS * CPR / NT;        // chunks per thread per tile
   static_assert(VPT >= 1 && ROWS * CPR % NT == 0, "split");
@@ -54,10 +54,10 @@ __global__ void __launch_bounds__(NT) tile_swap(char* a, const uint32_t* ys, int
       const int id = j * NT + threadIdx.x;
       const int row = id / CPR, c = id % CPR;
       if (ry != y) {
-        stg(a + row * stride + ry * R + c * 16, v0[j]);
-        stg(a + row * stride + y * R + c * 16, v1[j]);
+        stg(out + row * stride + ry * R + c * 16, v0[j]);
+        stg(out + row * stride + y * R + c * 16, v1[j]);
       } else {
-        stg(a + row * stride + y * R + c * 16, v0[j]);
+        stg(out + row * stride + y * R + c * 16, v0[j]);
       }
     }
   }
@@ -114,7 +114,8 @@ static uint32_t revb(uint32_t v, int m) {
 }
 
 template <int R, int NT, bool W256 = false, int ROWS = 64>
-void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
+void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm, char* out = nullptr) {
+  if (!out) out = a;  // in place unless a separate destination is given
   const uint64_t stride = total / ROWS;
   int m = 0;
   while (((uint64_t)R << (m + 1)) <= stride) ++m;
@@ -148,7 +149,7 @@ void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
     const int grid = sms * ctas_per_sm;
     auto launch = [&]() {
       if constexpr (W256) tile_swap256<R, ROWS, NT><<<grid, NT>>>(a, d_ys, np, m, stride);
-      else tile_swap<R, ROWS, NT><<<grid, NT>>>(a, d_ys, np, m, stride);
+      else tile_swap<R, ROWS, NT><<<grid, NT>>>(a, out, d_ys, np, m, stride);
     };
     for (int w = 0; w < 3; ++w) launch();
     std::vector<float> ts;
@@ -163,9 +164,9 @@ void run(char* a, uint32_t* d_ys, uint64_t total, int sms, int ctas_per_sm) {
     }
     std::sort(ts.begin(), ts.end());
     const uint64_t moved = 2 * (uint64_t)ROWS * R * n;
-    printf("{\"bytes\": %llu, \"rows\": %d, \"R\": %d, \"m\": %d, \"order\": %d, \"nt\": %d, \"ctas_per_sm\": %d, "
+    printf("{\"oop\": %d, \"bytes\": %llu, \"rows\": %d, \"R\": %d, \"m\": %d, \"order\": %d, \"nt\": %d, \"ctas_per_sm\": %d, "
            "\"w256\": %d, \"occ\": %d, \"gbs\": %.1f, \"best_gbs\": %.1f}\n",
-           (unsigned long long)total, ROWS, R, m, o, NT, ctas_per_sm, (int)W256, occ,
+           (int)(out != a), (unsigned long long)total, ROWS, R, m, o, NT, ctas_per_sm, (int)W256, occ,
            moved / ts[ts.size() / 2] / 1e6, moved / ts[0] / 1e6);
   }
 }
@@ -179,15 +180,16 @@ int main() {
     cudaMalloc(&a, total);
     cudaMalloc(&ys, (total / 64 / 256) * 4 + 1024);
     cudaMemset(a, 3, total);
-    run<512, 256>(a, ys, total, sms, 4);
-    run<512, 256, false, 64>(a, ys, total, sms, 2);
-    run<1024, 512, false, 32>(a, ys, total, sms, 2);
-    run<2048, 1024, false, 32>(a, ys, total, sms, 1);
-    run<2048, 512, false, 16>(a, ys, total, sms, 2);
-    run<2048, 1024, false, 16>(a, ys, total, sms, 1);
-    run<4096, 1024, false, 16>(a, ys, total, sms, 1);
-    run<4096, 1024, false, 8>(a, ys, total, sms, 1);
-    run<1024, 256, false, 16>(a, ys, total, sms, 4);
+    char* b2;
+    cudaMalloc(&b2, total);
+    cudaMemset(b2, 5, total);
+    for (int rep = 0; rep < 2; ++rep) {
+      run<512, 256>(a, ys, total, sms, 4);
+      run<512, 256>(a, ys, total, sms, 4, b2);
+      run<512, 256>(a, ys, total, sms, 2);
+      run<512, 256>(a, ys, total, sms, 2, b2);
+    }
+    cudaFree(b2);
     cudaFree(a);
     cudaFree(ys);
   }
