@@ -127,3 +127,17 @@ def test_fused_companion_watchdog_quiet_when_in_time():
     assert p.returncode == 0, p.stderr[-2000:]
     assert _json_lines(p.stdout) == []
     assert 'RETURNED {"value": 1.0}' in p.stdout
+
+
+def test_kernel_family_names_the_launch():
+    """bench.py labels roofline.kernel from the launch's (tile bits, path)."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    assert bench.kernel_family((6, 0), False) == "bitrev_oop_tile_kernel (Q=6)"
+    assert bench.kernel_family((7, 3), False) == "bitrev_oop_rect_kernel (QX=7)"
+    assert bench.kernel_family((4, 2), False).startswith("bitrev_ring_kernel (TMA tensor-map")
+    assert bench.kernel_family((6, 1), False).startswith("bitrev_ring_kernel (TMA bulk-row")
+    assert bench.kernel_family((6, 0), True) == "bitrev_inplace_tile_kernel (Q=6)"
+    assert bench.kernel_family((6, 6), True) == "bitrev_inplace_cluster_kernel (Q=6)"
+    assert bench.kernel_family((0, -3), False) == "bitrev_rows_kernel (short rows)"
