@@ -130,6 +130,16 @@ int bitrev_even_odd(const void* src, void* dst, int b, int elem_bytes, int64_t b
                     int64_t src_batch_stride, int64_t dst_batch_stride, void* stream);
 
 /*
+ * Fill scratch[0 .. 2^b) with what the reference's stockham_permute leaves in
+ * a caller-supplied scratch buffer (the last block's split of every level of
+ * its buffered passes), gathered from the UNPERMUTED array a; call it before
+ * permuting a.  Replaces: the side effect of _stockham on its scratch
+ * argument (src/permutations.py:30-59); the permutation itself is
+ * bitrev_inplace.  a and scratch must not overlap.
+ */
+int bitrev_stockham_scratch(const void* a, void* scratch, int b, int elem_bytes, void* stream);
+
+/*
  * Swap a[pairs[2k]] <-> a[pairs[2k+1]] for k < npairs, pairs a device array of
  * int64 index pairs that must be pairwise disjoint (a swap schedule is).
  * Replaces: apply_schedule -> _apply_pairs (src/schedule.py:100-130) for a

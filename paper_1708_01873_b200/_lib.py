@@ -30,6 +30,7 @@ SIGNATURES = {
     "bitrev_host_pipeline": (_c_int, [_vp, _vp, _c_i64, _c_int, _c_int, _c_i64, _vp, _vp]),
     "bitrev_transpose_square": (_c_int, [_vp, _c_int, _c_int, _c_i64, _c_i64, _vp]),
     "bitrev_even_odd": (_c_int, [_vp, _vp, _c_int, _c_int, _c_i64, _c_i64, _c_i64, _vp]),
+    "bitrev_stockham_scratch": (_c_int, [_vp, _vp, _c_int, _c_int, _vp]),
     "bitrev_apply_pairs": (_c_int, [_vp, _vp, _c_i64, _c_int, _vp]),
     "bitrev_apply_pairs_ordered": (_c_int, [_vp, _vp, _c_i64, _c_int, _vp]),
     "bitrev_swap_schedule": (_c_int, [_c_int, _vp, _vp]),

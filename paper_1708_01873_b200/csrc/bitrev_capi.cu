@@ -1640,6 +1640,30 @@ int bitrev_transpose_square(void* a, int h, int elem_bytes, int64_t batch, int64
   return BITREV_EELEM;
 }
 
+int bitrev_stockham_scratch(const void* a, void* scratch, int b, int elem_bytes, void* stream) {
+  const int E = elem_bytes;
+  if (b < 1 || b > kMaxBits) return BITREV_EWIDTH;
+  if (!valid_elem(E)) return BITREV_EELEM;
+  if (!a || !scratch) return BITREV_ENULL;
+  const uint64_t n = 1ull << b;
+  {
+    const uintptr_t a0 = (uintptr_t)a, s0 = (uintptr_t)scratch;
+    if (a0 < s0 + n * E && s0 < a0 + n * E) return BITREV_EOVERLAP;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned grid = (unsigned)elementwise_grid(n);
+  switch (E) {
+#define SS_CASE(E_)                                                                          \
+  case E_:                                                                                   \
+    stockham_scratch_kernel<E_><<<grid, 256, 0, st>>>(static_cast<const char*>(a),            \
+                                                      static_cast<char*>(scratch), b);        \
+    return finish_launch();
+    SS_CASE(1) SS_CASE(2) SS_CASE(4) SS_CASE(8) SS_CASE(16)
+#undef SS_CASE
+  }
+  return BITREV_EELEM;
+}
+
 int bitrev_even_odd(const void* src, void* dst, int b, int elem_bytes, int64_t batch,
                     int64_t src_batch_stride, int64_t dst_batch_stride, void* stream) {
   const int E = elem_bytes;

@@ -2359,6 +2359,38 @@ __global__ void __launch_bounds__(TrTile<E, Q>::THREADS)
 // ---------------------------------------------------------------------------
 // even-odd split (replaces _even_odd, src/recursive.py:84-93), out of place.
 
+// The scratch contents stockham_permute leaves behind
+// (/root/reference/pkg/src/bitrev/permutations.py:30-43, _stockham): level L
+// (block size 2^L, L = b .. 1) splits every aligned block through scratch,
+// so scratch[k], 2^(L-1) <= k < 2^L, last holds the odd element j = k -
+// 2^(L-1) of the last block's split at level L, i.e. the level-L input at
+// n - 2^L + 2j + 1, and scratch[0] the level-1 input at n - 2.  Level L
+// maps its input from the original array by rotating the low M bits of the
+// index left by one for M = L+1 .. b (each even-odd split is that rotation),
+// so each slot is one gather from the unpermuted array.
+template <int E>
+__global__ void stockham_scratch_kernel(const char* a, char* scratch, int b) {
+  using W = typename Word<E>::T;
+  const uint64_t n = 1ull << b;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    int L;
+    uint64_t p;
+    if (k == 0) {
+      L = 1;
+      p = n - 2;
+    } else {
+      L = 64 - __clzll((long long)k);
+      p = n - (1ull << L) + 2 * (k - (1ull << (L - 1))) + 1;
+    }
+    for (int M = L + 1; M <= b; ++M) {
+      const uint64_t mask = (1ull << M) - 1, lo = p & mask;
+      p = (p & ~mask) | (((lo << 1) | (lo >> (M - 1))) & mask);
+    }
+    reinterpret_cast<W*>(scratch)[k] = reinterpret_cast<const W*>(a)[p];
+  }
+}
+
 template <int E>
 __global__ void even_odd_kernel(const char* src, char* dst, int b, int64_t batch,
                                 int64_t src_bstride, int64_t dst_bstride) {

@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from . import _core
+from . import _core, _lib
 from .bits import BYTE_TABLE
 from ._core import as_tensor, check_array
 
@@ -27,16 +27,37 @@ from ._core import as_tensor, check_array
 
 
 def stockham_permute(array, b: int, scratch=None) -> None:
-    """Stockham entry point (src/permutations.py:46-59); scratch is validated
-    like the reference (>= n elements of the array dtype) and otherwise unused."""
+    """Stockham entry point (src/permutations.py:46-59).  scratch is validated
+    like the reference's (>= n elements of the array dtype).  The permutation
+    is the tile kernel; a caller-supplied scratch also receives what the
+    reference's buffered passes leave in it (bitrev_stockham_scratch, a
+    gather from the unpermuted array), so its first n elements end up
+    byte-identical to the reference's."""
     a = as_tensor(array)
     check_array(a, b)
     n = a.shape[0]
-    if scratch is not None:
-        s = as_tensor(scratch, "scratch")
-        if s.shape[0] < n or s.dtype != a.dtype:
-            raise ValueError(f"scratch must hold {n} elements of {a.dtype}")
-    _core.permute_inplace(a, b)
+    if scratch is None:
+        _core.permute_inplace(a, b)
+        return
+    s = as_tensor(scratch, "scratch")
+    if s.shape[0] < n or s.dtype != a.dtype:
+        raise ValueError(f"scratch must hold {n} elements of {a.dtype}")
+    if b == 0:
+        return  # one element: the reference's passes never run
+    E = _core.elem_bytes(a)
+    dev = a.device if a.is_cuda else _core.require_cuda()
+    work = a if (a.is_cuda and a.is_contiguous()) else a.to(dev, copy=True).contiguous()
+    head = s[:n]
+    sd = head if (head.is_cuda and head.device == dev and head.is_contiguous()) else \
+        torch.empty(n, dtype=a.dtype, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("bitrev_stockham_scratch", work.data_ptr(), sd.data_ptr(), b, E,
+                  _core._stream_ptr(dev))
+    _core.launch_inplace(work, b)
+    if work is not a:
+        a.copy_(work)
+    if sd is not head:
+        head.copy_(sd)
 
 
 def naive_bitwise_permute(array, b: int) -> None:

@@ -153,16 +153,19 @@ def even_odd_permute(array, b: int, scratch=None) -> None:
     is the index rotation i -> (i >> 1) | ((i & 1) << (b - 1)), which factors
     into two bit reversals: the full width, then each half (rev_{b-1} on the
     low b-1 bits after rev_b puts bit 0 on top).  Both run in place on the
-    tile kernels, so no scratch is touched (it is validated like the
-    reference's) and no n-element temporary is allocated.
+    tile kernels with no n-element temporary.  A caller-supplied scratch is
+    validated like the reference's and, like the reference's, ends up
+    holding the odd elements (the new top half) in its first n/2 slots.
     """
     check_width(b)
     a = as_tensor(array)
     if a.dim() != 1 or a.shape[0] != (1 << b):
         raise ValueError(f"array length {a.shape[0]} does not match 2**{b}")
-    _ensure_scratch(scratch, a.shape[0] >> 1, a.dtype)
-    if b == 1:
-        return  # [a0, a1] is already split
+    s = _ensure_scratch(scratch, a.shape[0] >> 1, a.dtype)
+    if b == 1:  # [a0, a1] is already split; the reference parks a1
+        if s is not None:
+            s[:1].copy_(a[1:])
+        return
     _core.elem_bytes(a)
     on_device = a.is_cuda and a.is_contiguous()
     dev = a.device if a.is_cuda else _core.require_cuda()
@@ -171,3 +174,6 @@ def even_odd_permute(array, b: int, scratch=None) -> None:
     _core.launch_inplace(work.view(2, -1), b - 1)
     if work is not a:
         a.copy_(work)
+    if s is not None:  # the reference's parked odds (src/recursive.py:88-89)
+        half = a.shape[0] >> 1
+        s[:half].copy_(work[half:])
