@@ -93,6 +93,30 @@ def _check_vs_device_oracle(x, out, b, base=0, total_bits=None):
         assert torch.equal(ow[s:s + c], xw.index_select(0, r)), f"mismatch in slots [{s}, {s + c})"
 
 
+@pytest.mark.parametrize("dtype,b,rows", [(torch.float64, 26, 1), (torch.float64, 28, 1),
+                                          (torch.complex128, 26, 1), (torch.complex128, 27, 1),
+                                          (torch.complex64, 16, 2048), (torch.float64, 20, 128)],
+                         ids=["f64-26", "f64-28", "c128-26", "c128-27", "c64-16x2048",
+                              "f64-20x128"])
+def test_spread_grid_launches_every_element(cuda, dtype, b, rows):
+    """Launches large enough for the spread grids (about 5 tiles per CTA
+    instead of a persistent grid: bitrev_capi.cu oop_grid), single arrays and
+    batched rows, every element against the device oracle."""
+    from paper_1708_01873_b200 import _lib
+
+    x = _random_bits(rows << b, dtype, cuda)
+    out = torch.empty_like(x)
+    if rows == 1:
+        br.cobra_out_of_place(x, out, br.CobraConfig(0), b)
+    else:
+        br.bitrev_batched(x.view(rows, 1 << b), b, out.view(rows, 1 << b))
+    torch.cuda.synchronize()
+    assert _lib.last_tile()[1] in (0, 3)  # the register tile families
+    for r in range(rows):
+        n = 1 << b
+        _check_vs_device_oracle(x[r * n:(r + 1) * n], out[r * n:(r + 1) * n], b)
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64, torch.complex128],
                          ids=["f32", "f64", "c128"])
 def test_cfg3_out_of_place_every_element(cuda, dtype):
