@@ -17,13 +17,14 @@ its top log2 N index bits, local reversal + NCCL all_to_all_single over
 NVLink + local interleave, with per-phase times and all-to-all bus bandwidth.
 The other configs are parity-test cases and --workload lines.
 
-Timing: W untimed warm-up steps, then EXACTLY K steps, each bracketed by CUDA
-events on the stream the kernel is launched on, with a barrier + device
-synchronise on both sides; the per-rank time is the sum of the K step
-durations and the job time is the max over ranks.  Workloads whose working
-set is below 4x the L2 get an L2 flush (a 512 MiB write) before every step,
-outside the step's events; the others (cfg3: 32 GiB per step) exceed the L2
-by two orders of magnitude.
+Timing: W untimed warm-up steps, then EXACTLY K steps timed with CUDA events
+on the stream the kernel is launched on, with a barrier + device synchronise
+on both sides; the job time is the max over ranks of the per-rank time.
+Workloads whose working set is below 4x the L2 get an L2 flush (a 512 MiB
+write) before every step, outside that step's own event pair, and the
+per-rank time is the sum of the K step durations; the others (cfg3: 32 GiB
+per step) exceed the L2 by two orders of magnitude and run their K steps back
+to back between one event pair.
 
 Under torchrun (N > 1) cfg1-cfg3 run one replica per rank ("replicas only":
 a single array does not shard without an exchange), cfg4 shards the batch
@@ -516,8 +517,22 @@ def kernel_family(chosen, inplace):
 
 
 def time_steps(torch, step, steps, stream, flush=None):
-    """Per-step seconds of `steps` steps, each bracketed by CUDA events on
-    `stream` (flush, if any, outside the events)."""
+    """Per-step seconds of `steps` steps timed with CUDA events on `stream`.
+
+    Without a flush the K steps run back to back between ONE event pair and
+    each step is credited K-th of the span (an event record between steps
+    costs ~3 us of device time, 2 % of cfg2's 181 us step:
+    tools/event_overhead_probe.py).  With an L2 flush every step has its own
+    event pair and the flush stays outside it."""
+    if flush is None:
+        s0 = torch.cuda.Event(enable_timing=True)
+        e0 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(steps):
+            step()
+        e0.record(stream)
+        torch.cuda.synchronize()
+        return [s0.elapsed_time(e0) / 1e3 / steps] * steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     for k in range(steps):
@@ -1097,7 +1112,10 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks,
         "step_ms": {"median": statistics.median(step_s) * 1e3, "min": min(step_s) * 1e3,
-                    "max": max(step_s) * 1e3, "all": [round(t * 1e3, 4) for t in step_s]},
+                    "max": max(step_s) * 1e3, "all": [round(t * 1e3, 4) for t in step_s],
+                    "method": ("one event pair around the K back-to-back steps"
+                               if flush is None else
+                               "an event pair per step, the L2 flush outside it")},
     }
     if sweep is not None:
         line["width_sweep"] = sweep
