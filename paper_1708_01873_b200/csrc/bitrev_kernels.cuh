@@ -694,6 +694,10 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
   };
 
   if constexpr (COMPACT) pc.start(a); else skip_fwd();
+  // programmatic dependent launch (a no-op unless the host sets the launch
+  // attribute): wait for the previous kernel in the stream -- typically the
+  // previous call on the same array -- to complete before the first load
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (!cur_valid()) return;
   issue();
   for (;;) {
@@ -707,6 +711,7 @@ __global__ void __launch_bounds__(Tile<E, Q>::THREADS, BITREV_MINB_IP)
     cur_next();
     const bool more = cur_valid();
     if (more) issue();
+    else asm volatile("griddepcontrol.launch_dependents;");  // last pair: let the next launch in
     char* base = a.dst + bi * a.dst_bstride;
     tile_drain<E, Q, BITREV_TILE_THREADS, CS>(U0, base + (ry << Q) * E, row_stride);
     if (pair) tile_drain<E, Q, BITREV_TILE_THREADS, CS>(U1, base + (y << Q) * E, row_stride);
