@@ -221,6 +221,37 @@ int prepare_kernel(K kernel, int threads, int smem_bytes) {
   return v;
 }
 
+// Programmatic dependent launch for the hot tile kernels: each kernel
+// triggers its dependents when a CTA reaches its last work item and waits
+// (griddepcontrol.wait) for its predecessor before its first load, so a
+// back-to-back call's launch and CTA start overlap the previous call's tail.
+// BITREV_B200_PDL=0 launches plainly (A/B runs).
+bool pdl_enabled() {
+  static const int v = env_int("BITREV_B200_PDL", 1);
+  return v != 0;
+}
+
+template <typename K, typename... Args>
+int launch_tiles(K kern, int grid, int threads, size_t smem, cudaStream_t st, Args... args) {
+  if (!pdl_enabled()) {
+    kern<<<grid, threads, smem, st>>>(args...);
+    return finish_launch();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+  if (e != cudaSuccess) return (int)e;
+  return finish_launch();
+}
+
 // ---------------------------------------------------------------------------
 // tile launches
 
@@ -296,8 +327,7 @@ int launch_oop_tile(const void* src, void* dst, int b, int64_t batch, int64_t sb
   a.npairs = 0;
   a.batch = batch;
   const int grid = oop_grid(E, a.ntiles, per_sm);
-  kern<<<grid, T::THREADS, T::BYTES, st>>>(a);
-  return finish_launch();
+  return launch_tiles(kern, grid, T::THREADS, T::BYTES, st, a);
 }
 
 template <int E, int Q, bool COMPACT>
@@ -316,29 +346,7 @@ int launch_ip_tile_mode(void* buf, int b, int64_t batch, int64_t bs, cudaStream_
   a.dst_bstride = bs * E;
   a.order = tile_order(true);
   const int grid = set_pair_work(a, batch, COMPACT, per_sm);
-  // Programmatic dependent launch: the kernel triggers its dependents when a
-  // CTA reaches its last pair and waits (griddepcontrol.wait) for its
-  // predecessor before its first load, so a back-to-back call's launch and
-  // CTA start overlap this call's tail: cfg2 5890-5911 -> 5957-5973 GB/s
-  // (+1.0 %), parity unchanged.  BITREV_B200_PDL=0 launches plainly (A/B).
-  static const int pdl = env_int("BITREV_B200_PDL", 1);
-  if (pdl) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(T::THREADS);
-    cfg.dynamicSmemBytes = 2 * T::BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-    if (e != cudaSuccess) return (int)e;
-    return finish_launch();
-  }
-  kern<<<grid, T::THREADS, 2 * T::BYTES, st>>>(a);
-  return finish_launch();
+  return launch_tiles(kern, grid, T::THREADS, 2 * T::BYTES, st, a);  // PDL: cfg2 +1.0 %
 }
 
 template <int E, int Q>
@@ -597,8 +605,7 @@ int launch_oop_rect(const void* src, void* dst, int b, int64_t batch, int64_t sb
   a.npairs = 0;
   a.batch = batch;
   const int grid = oop_grid(E, a.ntiles, per_sm);
-  kern<<<grid, T::THREADS, smem, st>>>(a);
-  return finish_launch();
+  return launch_tiles(kern, grid, T::THREADS, smem, st, a);
 }
 
 // Rectangular tiles: q selects the destination run (QX elements), rect_qz the

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, MINB)
   uint4 r[T::IPT][T::V];
 
   uint64_t t = blockIdx.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: predecessor done (no-op otherwise)
   if (t >= a.ntiles) return;
   auto src_tile = [&](uint64_t tt) {
     const uint64_t bi = tt >> a.m, y = work_to_y(tt & mmask, a.m, a.order);
@@ -390,6 +391,7 @@ __global__ void __launch_bounds__(Tile<E, Q, NT>::THREADS, MINB)
     __syncthreads();
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) tile_load<E, Q, true, NT, CS && BITREV_LD_CS>(r, src_tile(tn), row_stride);
+    else asm volatile("griddepcontrol.launch_dependents;");
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << Q) * E;
     tile_drain<E, Q, NT, CS>(smem, dbase, row_stride);
     if (tn >= a.ntiles) break;
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
   auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
 
   uint64_t t = blockIdx.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (no-op otherwise)
   if (t >= a.ntiles) return;
   load(t);
   for (;;) {
@@ -474,6 +477,7 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS)
     __syncthreads();
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) load(tn);
+    else asm volatile("griddepcontrol.launch_dependents;");
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
 #pragma unroll
     for (int it = 0; it < T::WPT; ++it) {
