@@ -1866,8 +1866,7 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     auto kern = stream_stores(16, b, batch) ? bitrev_fft_tile16_kernel<S_, true>         \
                                             : bitrev_fft_tile16_kernel<S_, false>;       \
     const int per_sm = prepare_kernel(kern, 256, kBytes);                                \
-    kern<<<fft_grid(a.ntiles, per_sm, S_ <= 3 ? 5 : 0), 256, kBytes, st>>>(fa);          \
-    return finish_launch();                                                              \
+    return launch_tiles(kern, fft_grid(a.ntiles, per_sm, S_ <= 3 ? 5 : 0), 256, kBytes, st, fa); \
   }
     switch (stages) { FFT16_LAUNCH(1) FFT16_LAUNCH(2) FFT16_LAUNCH(3) FFT16_LAUNCH(4) FFT16_LAUNCH(5) }
 #undef FFT16_LAUNCH
@@ -1917,8 +1916,7 @@ int bitrev_dit_prepass(const void* src, void* dst, int b, int elem_bytes, int64_
     using T = Rect<E_, QX_, QZ_>;                                                            \
     auto kern = bitrev_fft_rect_kernel<E_, QX_, QZ_, S_>;                                    \
     const int per_sm = prepare_kernel(kern, T::THREADS, T::BYTES);                           \
-    kern<<<fft_grid(a.ntiles, per_sm), T::THREADS, T::BYTES, st>>>(fa);                       \
-    return finish_launch();                                                                  \
+    return launch_tiles(kern, fft_grid(a.ntiles, per_sm), T::THREADS, T::BYTES, st, fa);     \
   }
   if (wide && qz == 5) {
     switch (stages) {

@@ -1776,6 +1776,7 @@ __global__ void __launch_bounds__(256, 1) bitrev_fft_tile16_kernel(FftArgs fa) {
   };
 
   uint64_t t = blockIdx.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (no-op otherwise)
   if (t >= a.ntiles) return;
   auto src_tile = [&](uint64_t tt) {
     const uint64_t bi = tt >> a.m, y = tt & mmask;
@@ -1788,6 +1789,7 @@ __global__ void __launch_bounds__(256, 1) bitrev_fft_tile16_kernel(FftArgs fa) {
     __syncthreads();
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) tile_load<16, 6, true, 256, CS && BITREV_LD_CS>(r, src_tile(tn), row_stride);
+    else asm volatile("griddepcontrol.launch_dependents;");
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << 6) * 16;
 #pragma unroll
     for (int it = 0; it < T::WPT; ++it) {
@@ -1852,6 +1854,7 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
   auto sidx = [&](int z, int col) { return z * T::GX + (col ^ ((z >> T::LV) & 7)); };
 
   uint64_t t = blockIdx.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL (no-op otherwise)
   if (t >= a.ntiles) return;
   load(t);
   __syncthreads();  // publish twq
@@ -1874,6 +1877,7 @@ __global__ void __launch_bounds__(Rect<E, QX, QZ>::THREADS,
     __syncthreads();
     const uint64_t tn = t + gridDim.x;
     if (tn < a.ntiles) load(tn);
+    else asm volatile("griddepcontrol.launch_dependents;");
     char* dbase = a.dst + bi * a.dst_bstride + (dev_rev(y, a.m) << QX) * E;
     if constexpr (kR8) fft_rows_drain_r8<QZ, STAGES, QX>(smem, dbase, dst_row, lt8, fa.inverse != 0);
     else fft_rows_drain_r4<E, (QX > 7 ? 7 : QX), QZ, STAGES>(smem, dbase, dst_row, lt, fa.inverse != 0);
